@@ -1,0 +1,287 @@
+/*
+ * vdfcg.h — C-ABI of the B200-native histogram -> weighted-GMM compression path.
+ *
+ * Drop-in boundary for the reference library `vdfc` (C++20, /root/reference/proj).
+ * Every entry point below replaces one reference function; the citation next to it
+ * names the reference interface (file:line, relative to proj/). Plain pointers and
+ * sizes only: no Eigen, no torch types.
+ *
+ * Matrix layouts follow the reference's Eigen defaults (column-major):
+ *   - particle velocities  N x d   -> velocity[a*N + n]  (SoA: u[N], v[N], w[N])
+ *   - Histogram2D::counts  n x n   -> counts[i + j*n]    (i = x bin, j = y bin)
+ *   - WeightedPoints::points N x d -> points[a*N + r]
+ *   - EStep::responsibilities M x N -> resp[i + n*M]
+ * Model parameters are component-major: weights[i], means[i*d + a],
+ * covariances[i*d*d + a*d + b] (symmetric, so row/col-major coincide).
+ *
+ * Pointers may be host (pageable or pinned) or device memory; each call detects
+ * the memory kind and stages host buffers through the context's stream. All
+ * compute runs in sm_100a kernels; there is no CPU fallback — without a usable
+ * CUDA device every compute call returns VDFCG_CUDA_ERROR.
+ *
+ * Errors mirror the reference's exception classes (return code + message from
+ * vdfcg_last_error(), thread-local). The C++ shim include/vdfcg.hpp rethrows them
+ * as std::invalid_argument / std::runtime_error / vdfc::CovarianceRepairError.
+ *
+ * Threading: a context owns one CUDA stream and a grow-only workspace; use one
+ * context per host thread (the reference is reentrant).
+ */
+#ifndef VDFCG_H
+#define VDFCG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VDFCG_ABI_VERSION 1
+
+/* Return codes. */
+enum {
+  VDFCG_OK = 0,
+  VDFCG_INVALID_ARGUMENT = 1, /* std::invalid_argument                        */
+  VDFCG_RUNTIME_ERROR = 2,    /* std::runtime_error                           */
+  VDFCG_REPAIR_FAILED = 3,    /* vdfc::CovarianceRepairError (types.hpp:99)   */
+  VDFCG_CUDA_ERROR = 4,       /* no device / launch failure                   */
+  VDFCG_CODEC_ERROR = 5       /* vdfc::CodecError (types.hpp:93)              */
+};
+
+/* Plane ids, identical to vdfc::Plane (types.hpp:18). */
+enum { VDFCG_PLANE_UV = 0, VDFCG_PLANE_VW = 1, VDFCG_PLANE_UW = 2, VDFCG_PLANE_NONE = 255 };
+
+/* Largest component count a fit may start with (FitConfig::initial_components). */
+#define VDFCG_MAX_COMPONENTS 16
+
+typedef struct vdfcg_ctx vdfcg_ctx;
+
+/* A GmmModel view (wgmm.hpp:27-39). Arrays are caller-owned. `scale`/`offset`
+ * carry the AffineMap (types.hpp:59-81); NULL means the identity map. */
+typedef struct vdfcg_model {
+  int32_t dimension;
+  int32_t components;
+  double* weights;     /* [components]           */
+  double* means;       /* [components * d]       */
+  double* covariances; /* [components * d * d]   */
+  double* scale;       /* [d] or NULL (identity) */
+  double* offset;      /* [d] or NULL (identity) */
+} vdfcg_model;
+
+/* FitConfig (wgmm.hpp:41-56). `warm_start` is a canonical (data-space) model or NULL. */
+typedef struct vdfcg_fit_config {
+  int32_t initial_components;   /* default 12   */
+  int32_t max_em_iterations;    /* default 100  */
+  double prune_threshold;       /* default 0.005 */
+  int32_t prune_check_interval; /* default 10   */
+  double loglik_rel_tolerance;  /* default 1e-6 */
+  uint64_t seed;                /* default 0    */
+  int32_t has_temperature;      /* 0: weighted variance of the points (wgmm.cpp:374) */
+  double temperature[3];        /* per-axis variance, data units */
+  const vdfcg_model* warm_start;
+} vdfcg_fit_config;
+
+/* FitResult (wgmm.hpp:64-70). Capacities are set by the caller. */
+typedef struct vdfcg_fit_result {
+  int32_t capacity_components; /* >= initial_components (or warm-start M) */
+  int32_t capacity_trace;      /* >= max_em_iterations */
+  vdfcg_model model;           /* out: canonical model, identity map (scale/offset ignored) */
+  double* loglik_trace;        /* [capacity_trace] */
+  int32_t trace_len;
+  int32_t iterations_used;
+  int32_t converged;
+  int32_t n_events;            /* pruning events, capacity = capacity_components */
+  int32_t* event_iteration;
+  int32_t* event_component;
+  double* event_weight;
+} vdfcg_fit_result;
+
+/* ModelMeta (codec.hpp:20-25). */
+typedef struct vdfcg_model_meta {
+  const char* species_label; /* UTF-8, not NUL-terminated necessarily */
+  int32_t label_len;
+  int32_t plane;             /* VDFCG_PLANE_* */
+  int64_t cycle;
+  double range_lo[3];
+  double range_hi[3];
+} vdfcg_model_meta;
+
+/* ------------------------------------------------------------------------- */
+/* Context, errors                                                            */
+/* ------------------------------------------------------------------------- */
+const char* vdfcg_last_error(void);
+int vdfcg_abi_version(void);
+int vdfcg_ctx_create(int device, vdfcg_ctx** out);
+int vdfcg_ctx_destroy(vdfcg_ctx* ctx);
+/* Use an external stream (e.g. torch.cuda.current_stream().cuda_stream). NULL restores the own stream. */
+int vdfcg_ctx_set_stream(vdfcg_ctx* ctx, void* cuda_stream);
+int vdfcg_ctx_synchronize(vdfcg_ctx* ctx);
+/* Per-kernel device timing (CUDA events on the context stream). When enabled, every
+ * kernel launch is bracketed by events; vdfcg_ctx_kernel_times reports, per kernel
+ * family, the summed milliseconds and launch count since the last reset. */
+int vdfcg_ctx_enable_timing(vdfcg_ctx* ctx, int enable);
+int vdfcg_ctx_reset_timing(vdfcg_ctx* ctx);
+int vdfcg_ctx_kernel_times(vdfcg_ctx* ctx, int32_t max_entries, char* names /* max_entries*32 */,
+                           double* ms, int64_t* launches, int32_t* n_entries);
+/* Total kernel launches issued by this context since creation. */
+int64_t vdfcg_ctx_launch_count(vdfcg_ctx* ctx);
+
+/* ------------------------------------------------------------------------- */
+/* Histogram (histogram.hpp / histogram.cpp)                                  */
+/* ------------------------------------------------------------------------- */
+
+/* bin_particles (histogram.hpp:48-49, histogram.cpp:45-76). velocities: N x d
+ * column-major; weights NULL = unit weights. counts: n_bins^2 column-major. */
+int vdfcg_bin_particles(vdfcg_ctx* ctx, const double* velocities, int64_t n, int32_t d,
+                        const double* weights, int32_t plane, int32_t n_bins, double xlo,
+                        double xhi, double ylo, double yhi, double* counts,
+                        double* out_of_range);
+
+/* all_planes (histogram.hpp:53, histogram.cpp:78-84): the uv, vw, uw marginals in
+ * ONE pass over the particles. counts3: 3 consecutive n_bins^2 column-major grids. */
+int vdfcg_all_planes(vdfcg_ctx* ctx, const double* velocities, int64_t n, int32_t d,
+                     const double* weights, int32_t n_bins, double lo, double hi,
+                     double* counts3, double* out_of_range3);
+
+/* to_weighted_points (histogram.hpp:55, histogram.cpp:86-109). `points` is
+ * count x 2 column-major with leading dimension = *count (the non-empty bin count
+ * when drop_empty, else n_bins^2); capacity bounds *count. */
+int vdfcg_to_weighted_points(vdfcg_ctx* ctx, const double* counts, int32_t n_bins, double xlo,
+                             double xhi, double ylo, double yhi, int32_t drop_empty,
+                             int64_t capacity, double* points, double* weights, int64_t* count,
+                             double* total_weight);
+
+/* ------------------------------------------------------------------------- */
+/* Weighted EM (wgmm.hpp / wgmm.cpp)                                          */
+/* ------------------------------------------------------------------------- */
+
+/* FitConfig::validate (wgmm.cpp:65-76); host-only, no device needed. */
+int vdfcg_validate_fit_config(const vdfcg_fit_config* cfg, int32_t dimension);
+
+/* normalize (wgmm.hpp:74, wgmm.cpp:78-100). out_points N x d column-major. */
+int vdfcg_normalize(vdfcg_ctx* ctx, const double* points, const double* weights, int64_t n,
+                    int32_t d, double* out_points, double* scale, double* offset);
+
+/* denormalize_model (wgmm.hpp:78, wgmm.cpp:102-120). out->scale/offset ignored. */
+int vdfcg_denormalize_model(vdfcg_ctx* ctx, const vdfcg_model* in, vdfcg_model* out);
+
+/* init_model (wgmm.hpp:85-86, wgmm.cpp:136-191). `normalized_points` N x d; the map is
+ * (scale, offset); out->components receives the (possibly reduced) M. */
+int vdfcg_init_model(vdfcg_ctx* ctx, const double* normalized_points, int64_t n, int32_t d,
+                     const vdfcg_fit_config* cfg, const double* temperature,
+                     const double* scale, const double* offset, vdfcg_model* out);
+
+/* e_step (wgmm.hpp:97, wgmm.cpp:233-255). MUTATES `model` covariances (in-place
+ * repair). resp: M x N column-major. unrepairable: capacity M. */
+int vdfcg_e_step(vdfcg_ctx* ctx, vdfcg_model* model, const double* points, const double* weights,
+                 int64_t n, double* resp, double* loglik, int32_t* unrepairable,
+                 int32_t* n_unrepairable);
+
+/* m_step (wgmm.hpp:106-107, wgmm.cpp:269-318). degenerate: capacity M (may be NULL). */
+int vdfcg_m_step(vdfcg_ctx* ctx, const double* points, const double* weights, int64_t n,
+                 double total_weight, const double* resp, const vdfcg_model* previous,
+                 vdfcg_model* out, int32_t* degenerate, int32_t* n_degenerate);
+
+/* prune_one (wgmm.hpp:112, wgmm.cpp:320-333). In place; *pruned = 1 when an event happened. */
+int vdfcg_prune_one(vdfcg_ctx* ctx, vdfcg_model* model, double threshold, int32_t iteration,
+                    int32_t* pruned, int32_t* event_component, double* event_weight);
+
+/* repair_covariance (wgmm.hpp:120, wgmm.cpp:340-362). doublings may be NULL. */
+int vdfcg_repair_covariance(vdfcg_ctx* ctx, const double* sigma, int32_t d, double* out,
+                            int32_t* doublings);
+
+/* fit (wgmm.hpp:126, wgmm.cpp:364-423). points N x d column-major. */
+int vdfcg_fit(vdfcg_ctx* ctx, const double* points, const double* weights, int64_t n, int32_t d,
+              double total_weight, const vdfcg_fit_config* cfg, vdfcg_fit_result* result);
+
+/* ------------------------------------------------------------------------- */
+/* Writer (codec.hpp / codec.cpp, FORMATS.md)                                  */
+/* ------------------------------------------------------------------------- */
+/* model_payload_bytes (codec.hpp:36, codec.cpp:86-89). */
+int64_t vdfcg_model_payload_bytes(int32_t components, int32_t dimension);
+/* Header bytes of a .gmmc record: 4+4+4+8+16d+2+L+4 (FORMATS.md:11-24). */
+int64_t vdfcg_model_header_bytes(int32_t dimension, int32_t label_len);
+/* encode_model (codec.hpp:48, codec.cpp:103-136). */
+int vdfcg_encode_model(vdfcg_ctx* ctx, const vdfcg_model* model, const vdfcg_model_meta* meta,
+                       uint8_t* out, int64_t capacity, int64_t* length);
+
+/* ------------------------------------------------------------------------- */
+/* Cell-batched path (new: the GPU generalisation of the per-subdomain fan-out, */
+/* pipeline.cpp:76-104,130-160,340-349; 3V bins per SURVEY.md Appendix A)      */
+/* ------------------------------------------------------------------------- */
+
+/* Particles of one species, grouped by spatial cell (PIC ownership order). */
+typedef struct vdfcg_cells {
+  int32_t dimension;            /* 2 or 3 velocity axes */
+  int64_t n_particles;
+  const double* velocity[3];    /* SoA axis arrays u, v, w; each n_particles */
+  const double* weights;        /* NULL = unit weights */
+  int32_t n_cells;
+  const int64_t* cell_offsets;  /* [n_cells+1]; cell c owns particles [off[c], off[c+1]) */
+  int32_t n_bins;               /* per axis; bins^d flat index (i*n+j)*n+k */
+  double lo[3];
+  double hi[3];
+} vdfcg_cells;
+
+/* Compacted per-cell histograms: cell c's non-empty bins, ascending flat key
+ * (= to_weighted_points(drop_empty) order), stored at [off[c], off[c]+nnz[c]). */
+typedef struct vdfcg_cell_bins {
+  int32_t* nnz;          /* [n_cells] */
+  uint32_t* keys;        /* [n_particles] */
+  double* counts;        /* [n_particles] */
+  double* out_of_range;  /* [n_cells] */
+  double* in_range;      /* [n_cells] (Histogram2D::in_range_count) */
+} vdfcg_cell_bins;
+
+/* Per-cell fit results, SoA with stride K = capacity_components. */
+typedef struct vdfcg_cell_results {
+  int32_t capacity_components;
+  int32_t capacity_trace;   /* 0: no trace stored */
+  int32_t* status;          /* [n_cells] VDFCG_* per cell */
+  int32_t* components;      /* [n_cells] M-hat */
+  int32_t* iterations;      /* [n_cells] */
+  int32_t* converged;       /* [n_cells] */
+  double* weights;          /* [n_cells*K] */
+  double* means;            /* [n_cells*K*d] */
+  double* covariances;      /* [n_cells*K*d*d] */
+  double* final_loglik;     /* [n_cells] last E-step loglik (fitting frame) */
+  double* loglik_trace;     /* [n_cells*capacity_trace] or NULL */
+  int32_t* n_events;        /* [n_cells] or NULL */
+  int32_t* event_iteration; /* [n_cells*K] or NULL */
+  int32_t* event_component; /* [n_cells*K] or NULL */
+  double* event_weight;     /* [n_cells*K] or NULL */
+} vdfcg_cell_results;
+
+/* Histogram every cell (bins^d, exact integer counts for unit weights). */
+int vdfcg_bin_cells(vdfcg_ctx* ctx, const vdfcg_cells* cells, vdfcg_cell_bins* out);
+
+/* Fit every cell's compacted histogram with the same FitConfig (pipeline.cpp:144 copies
+ * cfg.fit unchanged for every part). temperature: [d] or NULL (cfg / weighted variance). */
+int vdfcg_fit_cells(vdfcg_ctx* ctx, const vdfcg_cells* cells, const vdfcg_cell_bins* bins,
+                    const vdfcg_fit_config* cfg, vdfcg_cell_results* out);
+
+/* Pack every cell's fitted model as a .gmmc record (FORMATS.md). records: capacity
+ * bytes; record_offsets: [n_cells+1]. Cells with status != 0 get an empty record. */
+int vdfcg_pack_cells(vdfcg_ctx* ctx, int32_t n_cells, int32_t dimension,
+                     const vdfcg_cell_results* res, const vdfcg_model_meta* meta,
+                     uint8_t* records, int64_t capacity, int64_t* record_offsets);
+
+/* The whole compression step: bin_cells -> fit_cells (-> pack_cells when records != NULL),
+ * one stream, no host round trip in between. */
+int vdfcg_compress_cells(vdfcg_ctx* ctx, const vdfcg_cells* cells, const vdfcg_fit_config* cfg,
+                         vdfcg_cell_bins* bins, vdfcg_cell_results* out,
+                         const vdfcg_model_meta* meta, uint8_t* records, int64_t capacity,
+                         int64_t* record_offsets);
+
+/* Synthetic cell data for tests/bench (counter-based, deterministic per (seed, cell)):
+ * each cell draws from a 2-component mixture whose drift/temperature vary with the
+ * cell index. Device pointers only. */
+int vdfcg_synth_cells(vdfcg_ctx* ctx, int32_t dimension, int32_t n_cells,
+                      const int64_t* cell_offsets, uint64_t seed, int32_t species,
+                      double* velocity_u, double* velocity_v, double* velocity_w);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VDFCG_H */
