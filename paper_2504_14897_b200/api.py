@@ -1,0 +1,192 @@
+"""Product API: the reference's hot-path entry points, computed by libvdfcg.so.
+
+Function names, argument meaning and exceptions follow the reference
+(proj/include/vdfc/histogram.hpp, wgmm.hpp, codec.hpp). Every compute call goes
+through the C-ABI in include/vdfcg.h into sm_100a kernels; there is no CPU fallback —
+if the library cannot be loaded or no CUDA device exists, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from functools import partial
+
+import numpy as np
+
+from . import _abi, _marshal
+from .types import (AxisRange, FitConfig, GmmModel, InvalidArgument, ModelMeta,  # noqa: F401
+                    ParticleSet, WeightedPoints)
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libvdfcg.so")
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def _bind(lib) -> None:
+    vp, i32, i64, f64, u64 = C.c_void_p, C.c_int32, C.c_int64, C.c_double, C.c_uint64
+    sig = {
+        "vdfcg_last_error": (C.c_char_p, []),
+        "vdfcg_abi_version": (C.c_int, []),
+        "vdfcg_ctx_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
+        "vdfcg_ctx_destroy": (C.c_int, [vp]),
+        "vdfcg_ctx_set_stream": (C.c_int, [vp, vp]),
+        "vdfcg_ctx_synchronize": (C.c_int, [vp]),
+        "vdfcg_ctx_enable_timing": (C.c_int, [vp, C.c_int]),
+        "vdfcg_ctx_reset_timing": (C.c_int, [vp]),
+        "vdfcg_ctx_kernel_times": (C.c_int, [vp, i32, vp, vp, vp, vp]),
+        "vdfcg_ctx_launch_count": (i64, [vp]),
+        "vdfcg_bin_particles": (C.c_int, [vp, vp, i64, i32, vp, i32, i32, f64, f64, f64, f64, vp, vp]),
+        "vdfcg_all_planes": (C.c_int, [vp, vp, i64, i32, vp, i32, f64, f64, vp, vp]),
+        "vdfcg_to_weighted_points": (C.c_int, [vp, vp, i32, f64, f64, f64, f64, i32, i64, vp, vp, vp, vp]),
+        "vdfcg_validate_fit_config": (C.c_int, [vp, i32]),
+        "vdfcg_normalize": (C.c_int, [vp, vp, vp, i64, i32, vp, vp, vp]),
+        "vdfcg_denormalize_model": (C.c_int, [vp, vp, vp]),
+        "vdfcg_init_model": (C.c_int, [vp, vp, i64, i32, vp, vp, vp, vp, vp]),
+        "vdfcg_e_step": (C.c_int, [vp, vp, vp, vp, i64, vp, vp, vp, vp]),
+        "vdfcg_m_step": (C.c_int, [vp, vp, vp, i64, f64, vp, vp, vp, vp, vp]),
+        "vdfcg_prune_one": (C.c_int, [vp, vp, f64, i32, vp, vp, vp]),
+        "vdfcg_repair_covariance": (C.c_int, [vp, vp, i32, vp, vp]),
+        "vdfcg_fit": (C.c_int, [vp, vp, vp, i64, i32, f64, vp, vp]),
+        "vdfcg_model_payload_bytes": (i64, [i32, i32]),
+        "vdfcg_model_header_bytes": (i64, [i32, i32]),
+        "vdfcg_encode_model": (C.c_int, [vp, vp, vp, vp, i64, vp]),
+        "vdfcg_bin_cells": (C.c_int, [vp, vp, vp]),
+        "vdfcg_fit_cells": (C.c_int, [vp, vp, vp, vp, vp]),
+        "vdfcg_pack_cells": (C.c_int, [vp, i32, i32, vp, vp, vp, i64, vp]),
+        "vdfcg_compress_cells": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, i64, vp]),
+        "vdfcg_synth_cells": (C.c_int, [vp, i32, i32, vp, u64, i32, vp, vp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+
+
+def lib():
+    """The loaded CUDA library; raises (loudly) when it is missing."""
+    global _lib
+    if _lib is None:
+        with _lib_lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise RuntimeError(
+                        f"libvdfcg.so not built ({LIB_PATH}); run "
+                        "`python -m paper_2504_14897_b200.build` (there is no CPU fallback)")
+                lb = C.CDLL(LIB_PATH)
+                _bind(lb)
+                _lib = lb
+    return _lib
+
+
+def last_error() -> str:
+    return lib().vdfcg_last_error().decode()
+
+
+class Context:
+    """One CUDA stream + workspace on one device (vdfcg_ctx)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        _marshal.check(lib().vdfcg_ctx_create(device, C.byref(h)), last_error)
+        self.handle = h
+        self.device = device
+
+    def close(self) -> None:
+        if self.handle:
+            lib().vdfcg_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream_ptr: int | None) -> None:
+        _marshal.check(lib().vdfcg_ctx_set_stream(self.handle, stream_ptr), last_error)
+
+    def synchronize(self) -> None:
+        _marshal.check(lib().vdfcg_ctx_synchronize(self.handle), last_error)
+
+    def enable_timing(self, on: bool = True) -> None:
+        _marshal.check(lib().vdfcg_ctx_enable_timing(self.handle, 1 if on else 0), last_error)
+
+    def reset_timing(self) -> None:
+        _marshal.check(lib().vdfcg_ctx_reset_timing(self.handle), last_error)
+
+    def kernel_times(self) -> dict:
+        """{kernel family: (total ms, launches)} from CUDA events on the context stream."""
+        n = 64
+        names = C.create_string_buffer(32 * n)
+        ms = np.zeros(n)
+        cnt = np.zeros(n, dtype=np.int64)
+        k = C.c_int32(0)
+        _marshal.check(lib().vdfcg_ctx_kernel_times(self.handle, n, names, ms.ctypes.data,
+                                                    cnt.ctypes.data, C.byref(k)), last_error)
+        out = {}
+        for i in range(k.value):
+            nm = names.raw[32 * i:32 * (i + 1)].split(b"\0", 1)[0].decode()
+            out[nm] = (float(ms[i]), int(cnt[i]))
+        return out
+
+    def launch_count(self) -> int:
+        return int(lib().vdfcg_ctx_launch_count(self.handle))
+
+
+_tls = threading.local()
+
+
+def context(device: int | None = None) -> Context:
+    """Per-thread, per-device default context (the reference API is reentrant)."""
+    if device is None:
+        device = int(os.environ.get("VDFCG_DEVICE", getattr(_tls, "device", 0)))
+    cache = getattr(_tls, "ctxs", None)
+    if cache is None:
+        cache = _tls.ctxs = {}
+    if device not in cache:
+        cache[device] = Context(device)
+    return cache[device]
+
+
+def _call(name, *args):
+    return getattr(lib(), "vdfcg_" + name)(context().handle, *args)
+
+
+def _err():
+    return last_error()
+
+
+# ---------------------------------------------------------------------------- API
+bin_particles = partial(_marshal.bin_particles, _call, _err)
+bin_particles.__doc__ = "histogram.hpp:48-49 bin_particles(particles, plane, n_bins, range_x, range_y)"
+all_planes = partial(_marshal.all_planes, _call, _err)
+to_weighted_points = partial(_marshal.to_weighted_points, _call, _err)
+normalize = partial(_marshal.normalize, _call, _err)
+denormalize_model = partial(_marshal.denormalize_model, _call, _err)
+init_model = partial(_marshal.init_model, _call, _err)
+e_step = partial(_marshal.e_step, _call, _err)
+m_step = partial(_marshal.m_step, _call, _err)
+prune_one = partial(_marshal.prune_one, _call, _err)
+prune = partial(_marshal.prune, _call, _err)
+repair_covariance = partial(_marshal.repair_covariance, _call, _err)
+fit = partial(_marshal.fit, _call, _err)
+encode_model = partial(_marshal.encode_model, _call, _err)
+model_payload_bytes = _marshal.model_payload_bytes
+
+
+def default_axis_range(particles: ParticleSet, axis: int) -> AxisRange:
+    """histogram.cpp:27-30: +/- 5 nominal thermal speeds."""
+    vth = float(np.sqrt(particles.nominal_temperature[axis]))
+    return AxisRange(-5.0 * vth, 5.0 * vth)
+
+
+def validate_fit_config(config: FitConfig, d: int) -> None:
+    """FitConfig::validate (wgmm.cpp:65-76); host-only."""
+    cfg = _abi.fit_config_struct(config, d)
+    _marshal.check(lib().vdfcg_validate_fit_config(C.byref(cfg), d), last_error)
+
+
+from .cells import (CellBatch, bin_cells, compress_cells, fit_cells, pack_cells,  # noqa: E402,F401
+                    synth_cells)

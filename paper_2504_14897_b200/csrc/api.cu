@@ -1,0 +1,879 @@
+// api.cu — the extern "C" entry points of include/vdfcg.h. Host code here only
+// validates arguments (the reference's precondition checks and messages), stages host
+// buffers through the context stream and launches the sm_100a kernels; every number the
+// API returns is computed on the device.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "ctx.cuh"
+#include "em.cuh"
+#include "em_entry.cuh"
+#include "hist.cuh"
+#include "pack.cuh"
+
+namespace vdfcg {
+void launch_synth(vdfcg_ctx* ctx, int d, int n_cells, const int64_t* offsets, uint64_t seed,
+                  int species, double* u, double* v, double* w);
+
+namespace {
+
+void begin(vdfcg_ctx* ctx) {
+  if (!ctx) throw InvalidArgument("null vdfcg context");
+  VDFCG_CUDA(cudaSetDevice(ctx->device));
+  arena_reset(ctx);
+}
+
+bool range_ok(double lo, double hi) { return std::isfinite(lo) && std::isfinite(hi) && lo < hi; }
+
+const char* plane_name(int p) { return p == 0 ? "uv" : p == 1 ? "vw" : "uw"; }
+
+void plane_axes(int plane, int* ax, int* ay) {
+  switch (plane) {
+    case 0: *ax = 0; *ay = 1; return;
+    case 1: *ax = 1; *ay = 2; return;
+    case 2: *ax = 0; *ay = 2; return;
+    default: throw InvalidArgument("unknown plane id " + std::to_string(plane));
+  }
+}
+
+// FitConfig::validate (wgmm.cpp:65-76)
+void validate_config(const vdfcg_fit_config* cfg, int d) {
+  if (!cfg) throw InvalidArgument("null fit config");
+  if (cfg->initial_components < 1) throw InvalidArgument("initial_components must be >= 1");
+  if (cfg->initial_components > VDFCG_MAX_COMPONENTS)
+    throw InvalidArgument("initial_components must be <= 16 on this implementation");
+  if (cfg->max_em_iterations < 1) throw InvalidArgument("max_em_iterations must be >= 1");
+  if (!(cfg->prune_threshold > 0.0)) throw InvalidArgument("prune_threshold must be > 0");
+  if (cfg->prune_threshold >= 1.0 / cfg->initial_components)
+    throw InvalidArgument("prune_threshold must be < 1/initial_components");
+  if (cfg->prune_check_interval < 1) throw InvalidArgument("prune_check_interval must be >= 1");
+  if (!(cfg->loglik_rel_tolerance > 0.0))
+    throw InvalidArgument("loglik_rel_tolerance must be > 0");
+  if (cfg->has_temperature)
+    for (int a = 0; a < d; ++a)
+      if (!(cfg->temperature[a] > 0.0))
+        throw InvalidArgument("temperature must be > 0 on every axis");
+  if (cfg->warm_start) {
+    if (cfg->warm_start->dimension != d)
+      throw InvalidArgument("warm-start model dimension does not match the data");
+    if (cfg->warm_start->components < 1 || cfg->warm_start->components > VDFCG_MAX_COMPONENTS)
+      throw InvalidArgument("warm-start model must have 1..16 components");
+  }
+}
+
+// Device-side EmConfig: uniforms from mt19937_64(seed) and the canonical warm model.
+EmConfig make_em_config(vdfcg_ctx* ctx, const vdfcg_fit_config* cfg, int d) {
+  EmConfig e{};
+  e.M = cfg->initial_components;
+  e.max_it = cfg->max_em_iterations;
+  e.prune_thr = cfg->prune_threshold;
+  e.interval = cfg->prune_check_interval;
+  e.tol = cfg->loglik_rel_tolerance;
+  e.has_temp = cfg->has_temperature ? 1 : 0;
+  for (int a = 0; a < 3; ++a) e.temp[a] = cfg->temperature[a];
+  double* u = arena<double>(ctx, 64);
+  launch_mt_uniforms(ctx, cfg->seed, VDFCG_MAX_COMPONENTS * 3, u);
+  e.uniforms = u;
+  if (cfg->warm_start) {
+    const vdfcg_model* w = cfg->warm_start;
+    const int m = w->components;
+    auto sw = stage_in(ctx, w->weights, m);
+    auto smu = stage_in(ctx, w->means, size_t(m) * d);
+    auto scv = stage_in(ctx, w->covariances, size_t(m) * d * d);
+    auto ssc = stage_in(ctx, w->scale, w->scale ? d : 0);
+    auto sof = stage_in(ctx, w->offset, w->offset ? d : 0);
+    double* ow = arena<double>(ctx, m);
+    double* omu = arena<double>(ctx, size_t(m) * d);
+    double* ocv = arena<double>(ctx, size_t(m) * d * d);
+    launch_canonicalize(ctx, d, m, sw.dev, smu.dev, scv.dev, (w->scale && w->offset) ? ssc.dev : nullptr,
+                        (w->scale && w->offset) ? sof.dev : nullptr, ow, omu, ocv);
+    e.warm_m = m;
+    e.warm_w = ow;
+    e.warm_mu = omu;
+    e.warm_cov = ocv;
+  }
+  return e;
+}
+
+template <class T>
+void copy_out(vdfcg_ctx* ctx, T* dst, const T* src, size_t count) {
+  if (dst && count)
+    VDFCG_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDefault, ctx->stream));
+}
+
+template <class T>
+T read_scalar(vdfcg_ctx* ctx, const T* dev) {
+  T* h = static_cast<T*>(ctx->pinned);
+  VDFCG_CUDA(cudaMemcpyAsync(h, dev, sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  return *h;
+}
+
+struct EmOutDev {
+  EmOut o;
+  std::vector<int> dummy;
+};
+
+EmOut alloc_em_out(vdfcg_ctx* ctx, int n_cells, int d, int K, int trace_cap, bool events) {
+  EmOut o{};
+  o.K = K;
+  o.trace_cap = trace_cap;
+  o.status = arena<int32_t>(ctx, n_cells);
+  o.comps = arena<int32_t>(ctx, n_cells);
+  o.iters = arena<int32_t>(ctx, n_cells);
+  o.conv = arena<int32_t>(ctx, n_cells);
+  o.w = arena<double>(ctx, size_t(n_cells) * K);
+  o.mu = arena<double>(ctx, size_t(n_cells) * K * d);
+  o.cov = arena<double>(ctx, size_t(n_cells) * K * d * d);
+  o.final_ll = arena<double>(ctx, n_cells);
+  o.trace = trace_cap > 0 ? arena<double>(ctx, size_t(n_cells) * trace_cap) : nullptr;
+  if (events) {
+    o.n_events = arena<int32_t>(ctx, n_cells);
+    o.ev_it = arena<int32_t>(ctx, size_t(n_cells) * K);
+    o.ev_comp = arena<int32_t>(ctx, size_t(n_cells) * K);
+    o.ev_w = arena<double>(ctx, size_t(n_cells) * K);
+  }
+  o.err_axis = arena<int32_t>(ctx, n_cells);
+  o.err_value = arena<double>(ctx, n_cells);
+  return o;
+}
+
+void throw_status(int status, int err_id, double err_value, bool fit_prefix) {
+  const std::string msg = prologue_message(status, err_id, err_value, fit_prefix);
+  if (status == VDFCG_INVALID_ARGUMENT) throw InvalidArgument(msg);
+  if (status == VDFCG_REPAIR_FAILED) throw RepairFailed(msg);
+  throw RuntimeError(msg);
+}
+
+CellsDev stage_cells(vdfcg_ctx* ctx, const vdfcg_cells* cells) {
+  if (!cells) throw InvalidArgument("null cells");
+  const int d = cells->dimension;
+  if (d != 2 && d != 3) throw InvalidArgument("particle dimension must be 2 or 3");
+  if (cells->n_bins < 2) throw InvalidArgument("n_bins must be >= 2");
+  double nbd = 1.0;
+  for (int a = 0; a < d; ++a) nbd *= cells->n_bins;
+  if (nbd > 2147483647.0) throw InvalidArgument("n_bins^d must fit a 31-bit bin key");
+  for (int a = 0; a < d; ++a)
+    if (!range_ok(cells->lo[a], cells->hi[a]))
+      throw InvalidArgument("axis range must satisfy min < max");
+  if (cells->n_cells < 0 || cells->n_particles < 0) throw InvalidArgument("negative sizes");
+  if (!cells->cell_offsets) throw InvalidArgument("cell_offsets is required");
+  CellsDev c{};
+  c.d = d;
+  c.n = cells->n_particles;
+  for (int a = 0; a < d; ++a) {
+    if (!cells->velocity[a] && c.n) throw InvalidArgument("missing velocity axis");
+    c.vel[a] = stage_in(ctx, cells->velocity[a], c.n).dev;
+  }
+  for (int a = d; a < 3; ++a) c.vel[a] = c.vel[0];
+  c.w = cells->weights ? stage_in(ctx, cells->weights, c.n).dev : nullptr;
+  c.n_cells = cells->n_cells;
+  c.offsets = stage_in(ctx, cells->cell_offsets, size_t(c.n_cells) + 1).dev;
+  c.n_bins = cells->n_bins;
+  for (int a = 0; a < 3; ++a) {
+    c.lo[a] = cells->lo[a];
+    c.hi[a] = cells->hi[a];
+  }
+  return c;
+}
+
+PackMeta make_pack_meta(vdfcg_ctx* ctx, const vdfcg_model_meta* meta, int d) {
+  if (!meta) throw InvalidArgument("null model meta");
+  if (meta->label_len < 0 || meta->label_len > 0xffff) throw InvalidArgument("species label too long");
+  PackMeta pm{};
+  pm.d = d;
+  pm.plane = (meta->plane >= 0 && meta->plane <= 2) ? meta->plane : 255;
+  pm.cycle = meta->cycle;
+  for (int a = 0; a < 3; ++a) {
+    pm.lo[a] = meta->range_lo[a];
+    pm.hi[a] = meta->range_hi[a];
+  }
+  pm.label_len = meta->label_len;
+  uint8_t* lab = arena<uint8_t>(ctx, std::max(meta->label_len, 1));
+  if (meta->label_len)
+    VDFCG_CUDA(cudaMemcpyAsync(lab, meta->species_label, meta->label_len, cudaMemcpyDefault, ctx->stream));
+  pm.label = lab;
+  return pm;
+}
+
+// GmmModel::validate (wgmm.cpp:46-63) on the device.
+__global__ void validate_model_kernel(int d, int m, const double* w, const double* cov, int* code) {
+  if (threadIdx.x != 0) return;
+  int c = 0;
+  if (m < 1) c = 1;
+  double total = 0.0;
+  for (int i = 0; i < m && !c; ++i) {
+    if (!(w[i] > 0.0)) c = 2;
+    for (int a = 0; a < d && !c; ++a)
+      for (int b = 0; b < d; ++b)
+        if (!(cov[(i * d + a) * d + b] == cov[(i * d + b) * d + a])) c = 3;
+    total = __dadd_rn(total, w[i]);
+  }
+  if (!c && fabs(total - 1.0) > 1e-12) c = 4;
+  *code = c;
+}
+
+}  // namespace
+}  // namespace vdfcg
+
+using namespace vdfcg;
+
+extern "C" {
+
+int vdfcg_validate_fit_config(const vdfcg_fit_config* cfg, int32_t d) {
+  return guard_impl([&] { validate_config(cfg, d); });
+}
+
+int64_t vdfcg_model_payload_bytes(int32_t m, int32_t d) { return payload_bytes(m, d); }
+int64_t vdfcg_model_header_bytes(int32_t d, int32_t l) { return header_bytes(d, l); }
+
+// ------------------------------------------------------------------ histogram
+int vdfcg_bin_particles(vdfcg_ctx* ctx, const double* velocities, int64_t n, int32_t d,
+                        const double* weights, int32_t plane, int32_t n_bins, double xlo,
+                        double xhi, double ylo, double yhi, double* counts, double* oor) {
+  return guard_impl([&] {
+    begin(ctx);
+    if (d != 2 && d != 3) throw InvalidArgument("particle dimension must be 2 or 3");
+    if (n_bins < 2) throw InvalidArgument("n_bins must be >= 2");
+    if (!range_ok(xlo, xhi) || !range_ok(ylo, yhi))
+      throw InvalidArgument("axis range must satisfy min < max");
+    int ax, ay;
+    plane_axes(plane, &ax, &ay);
+    if (ay >= d)
+      throw InvalidArgument(std::string("plane ") + plane_name(plane) +
+                            " requires the w axis, but particles are " + std::to_string(d) +
+                            "-dimensional");
+    if (!counts || !oor) throw InvalidArgument("null output");
+    auto v = stage_in(ctx, velocities, size_t(n) * d);
+    auto w = stage_in(ctx, weights, weights ? size_t(n) : 0);
+    const size_t nn = size_t(n_bins) * n_bins;
+    auto c = stage_out(ctx, counts, nn);
+    auto o = stage_out(ctx, oor, 1);
+    launch_hist2d(ctx, v.dev, n, d, weights ? w.dev : nullptr, 1, &ax, &ay, n_bins, &xlo, &xhi,
+                  &ylo, &yhi, c.dev, o.dev);
+    finish(ctx, c);
+    finish(ctx, o);
+    sync(ctx);
+  });
+}
+
+int vdfcg_all_planes(vdfcg_ctx* ctx, const double* velocities, int64_t n, int32_t d,
+                     const double* weights, int32_t n_bins, double lo, double hi, double* counts3,
+                     double* oor3) {
+  return guard_impl([&] {
+    begin(ctx);
+    if (d != 3) throw InvalidArgument("all_planes requires d=3 particles; use bin_particles for d=2");
+    if (n_bins < 2) throw InvalidArgument("n_bins must be >= 2");
+    if (!range_ok(lo, hi)) throw InvalidArgument("axis range must satisfy min < max");
+    auto v = stage_in(ctx, velocities, size_t(n) * d);
+    auto w = stage_in(ctx, weights, weights ? size_t(n) : 0);
+    const size_t nn = size_t(n_bins) * n_bins;
+    auto c = stage_out(ctx, counts3, 3 * nn);
+    auto o = stage_out(ctx, oor3, 3);
+    const int ax[3] = {0, 1, 0}, ay[3] = {1, 2, 2};
+    const double l3[3] = {lo, lo, lo}, h3[3] = {hi, hi, hi};
+    launch_hist2d(ctx, v.dev, n, d, weights ? w.dev : nullptr, 3, ax, ay, n_bins, l3, h3, l3, h3,
+                  c.dev, o.dev);
+    finish(ctx, c);
+    finish(ctx, o);
+    sync(ctx);
+  });
+}
+
+int vdfcg_to_weighted_points(vdfcg_ctx* ctx, const double* counts, int32_t n_bins, double xlo,
+                             double xhi, double ylo, double yhi, int32_t drop_empty,
+                             int64_t capacity, double* points, double* weights, int64_t* count,
+                             double* total_weight) {
+  return guard_impl([&] {
+    begin(ctx);
+    if (n_bins < 1) throw InvalidArgument("n_bins must be >= 1");
+    if (!count || !total_weight) throw InvalidArgument("null output");
+    const size_t nn = size_t(n_bins) * n_bins;
+    auto c = stage_in(ctx, counts, nn);
+    const size_t cap = static_cast<size_t>(std::max<int64_t>(capacity, 0));
+    double* pd = arena<double>(ctx, 2 * cap);
+    double* wd = arena<double>(ctx, cap);
+    double* td = arena<double>(ctx, 1);
+    const int64_t k = launch_to_weighted_points(ctx, c.dev, n_bins, xlo, xhi, ylo, yhi,
+                                                drop_empty != 0, capacity, pd, wd, td);
+    const double tot = read_scalar(ctx, td);
+    if (!(tot > 0.0)) throw InvalidArgument("degenerate histogram: no in-range weight");
+    if (k > capacity) throw InvalidArgument("to_weighted_points: capacity too small");
+    copy_out(ctx, points, pd, size_t(2 * k));
+    copy_out(ctx, weights, wd, size_t(k));
+    sync(ctx);
+    *count = k;
+    *total_weight = tot;
+  });
+}
+
+// ------------------------------------------------------------------ EM entry points
+int vdfcg_normalize(vdfcg_ctx* ctx, const double* points, const double* weights, int64_t n,
+                    int32_t d, double* out_points, double* scale, double* offset) {
+  return guard_impl([&] {
+    begin(ctx);
+    if (d < 2 || d > 3) throw InvalidArgument("dimension must be 2 or 3");
+    auto p = stage_in(ctx, points, size_t(n) * d);
+    auto w = stage_in(ctx, weights, size_t(n));
+    EmConfig cfg{};
+    cfg.has_temp = 1;
+    cfg.warm_m = 1;  // skips temperature + distinct count: normalize only
+    double* z = arena<double>(ctx, size_t(std::max<int64_t>(n, 1)) * d);
+    Frame* fr = arena<Frame>(ctx, 1);
+    launch_fit_prologue(ctx, d, p.dev, w.dev, n, 0.0, cfg, z, fr);
+    Frame F;
+    VDFCG_CUDA(cudaMemcpyAsync(&F, fr, sizeof(Frame), cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    if (F.status) throw_status(F.status, F.err_axis, F.err_value, false);
+    copy_out(ctx, out_points, z, size_t(n) * d);
+    sync(ctx);
+    for (int a = 0; a < d; ++a) {
+      scale[a] = F.scale[a];
+      offset[a] = F.offset[a];
+    }
+  });
+}
+
+int vdfcg_denormalize_model(vdfcg_ctx* ctx, const vdfcg_model* in, vdfcg_model* out) {
+  return guard_impl([&] {
+    begin(ctx);
+    if (!in || !out) throw InvalidArgument("null model");
+    const int d = in->dimension, m = in->components;
+    auto w = stage_in(ctx, in->weights, m);
+    auto mu = stage_in(ctx, in->means, size_t(m) * d);
+    auto cv = stage_in(ctx, in->covariances, size_t(m) * d * d);
+    const bool map = in->scale && in->offset;
+    auto sc = stage_in(ctx, in->scale, map ? d : 0);
+    auto of = stage_in(ctx, in->offset, map ? d : 0);
+    double* ow = arena<double>(ctx, m);
+    double* omu = arena<double>(ctx, size_t(m) * d);
+    double* ocv = arena<double>(ctx, size_t(m) * d * d);
+    launch_canonicalize(ctx, d, m, w.dev, mu.dev, cv.dev, map ? sc.dev : nullptr, map ? of.dev : nullptr,
+                        ow, omu, ocv);
+    copy_out(ctx, out->weights, ow, m);
+    copy_out(ctx, out->means, omu, size_t(m) * d);
+    copy_out(ctx, out->covariances, ocv, size_t(m) * d * d);
+    sync(ctx);
+    out->dimension = d;
+    out->components = m;
+    if (out->scale && out->offset)
+      for (int a = 0; a < d; ++a) {
+        out->scale[a] = 1.0;
+        out->offset[a] = 0.0;
+      }
+  });
+}
+
+int vdfcg_init_model(vdfcg_ctx* ctx, const double* normalized_points, int64_t n, int32_t d,
+                     const vdfcg_fit_config* cfg, const double* temperature, const double* scale,
+                     const double* offset, vdfcg_model* out) {
+  return guard_impl([&] {
+    begin(ctx);
+    validate_config(cfg, d);
+    if (!scale || !offset || !out) throw InvalidArgument("null argument");
+    if (!cfg->warm_start) {
+      for (int a = 0; a < d; ++a)
+        if (!(temperature[a] > 0.0))
+          throw InvalidArgument("temperature must be a positive per-axis variance");
+    }
+    EmConfig e = make_em_config(ctx, cfg, d);
+    Frame F{};
+    for (int a = 0; a < d; ++a) {
+      F.scale[a] = scale[a];
+      F.offset[a] = offset[a];
+      F.temp[a] = temperature ? temperature[a] : 1.0;
+    }
+    auto z = stage_in(ctx, normalized_points, size_t(n) * d);
+    const int K = std::max(cfg->initial_components, e.warm_m);
+    double* w = arena<double>(ctx, K);
+    double* mu = arena<double>(ctx, size_t(K) * d);
+    double* cv = arena<double>(ctx, size_t(K) * d * d);
+    int* m = arena<int>(ctx, 1);
+    launch_init_model(ctx, d, z.dev, n, e, F, w, mu, cv, m);
+    const int M = read_scalar(ctx, m);
+    copy_out(ctx, out->weights, w, M);
+    copy_out(ctx, out->means, mu, size_t(M) * d);
+    copy_out(ctx, out->covariances, cv, size_t(M) * d * d);
+    sync(ctx);
+    out->dimension = d;
+    out->components = M;
+    if (out->scale && out->offset)
+      for (int a = 0; a < d; ++a) {
+        out->scale[a] = scale[a];
+        out->offset[a] = offset[a];
+      }
+  });
+}
+
+int vdfcg_e_step(vdfcg_ctx* ctx, vdfcg_model* model, const double* points, const double* weights,
+                 int64_t n, double* resp, double* loglik, int32_t* unrepairable,
+                 int32_t* n_unrepairable) {
+  return guard_impl([&] {
+    begin(ctx);
+    if (!model) throw InvalidArgument("null model");
+    const int d = model->dimension, m = model->components;
+    if (d < 1 || d > 3) throw InvalidArgument("model dimension must be 1..3");
+    if (m < 1 || m > VDFCG_MAX_COMPONENTS) throw InvalidArgument("model must have 1..16 components");
+    auto w = stage_in(ctx, model->weights, m);
+    auto mu = stage_in(ctx, model->means, size_t(m) * d);
+    auto cv = stage_in(ctx, model->covariances, size_t(m) * d * d);
+    auto x = stage_in(ctx, points, size_t(n) * d);
+    auto pw = stage_in(ctx, weights, size_t(n));
+    double* r = arena<double>(ctx, size_t(m) * n);
+    double* ll = arena<double>(ctx, 1);
+    int* dead = arena<int>(ctx, VDFCG_MAX_COMPONENTS);
+    int* nd = arena<int>(ctx, 1);
+    if (d == 1) throw InvalidArgument("e_step supports d = 2 or 3");
+    launch_e_step(ctx, d, m, w.dev, mu.dev, cv.dev, x.dev, pw.dev, n, r, ll, dead, nd);
+    const int ndead = read_scalar(ctx, nd);
+    if (ndead == m) throw RuntimeError("all mixture components are degenerate");
+    copy_out(ctx, resp, r, size_t(m) * n);
+    copy_out(ctx, model->covariances, cv.dev, size_t(m) * d * d);  // in-place repair
+    std::vector<int> dl(VDFCG_MAX_COMPONENTS);
+    VDFCG_CUDA(cudaMemcpyAsync(dl.data(), dead, sizeof(int) * VDFCG_MAX_COMPONENTS, cudaMemcpyDeviceToHost, ctx->stream));
+    double llh = 0.0;
+    VDFCG_CUDA(cudaMemcpyAsync(&llh, ll, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    *loglik = llh;
+    for (int i = 0; i < ndead; ++i) unrepairable[i] = dl[i];
+    *n_unrepairable = ndead;
+  });
+}
+
+int vdfcg_m_step(vdfcg_ctx* ctx, const double* points, const double* weights, int64_t n,
+                 double total_weight, const double* resp, const vdfcg_model* previous,
+                 vdfcg_model* out, int32_t* degenerate, int32_t* n_degenerate) {
+  return guard_impl([&] {
+    begin(ctx);
+    if (!previous || !out) throw InvalidArgument("null model");
+    const int d = previous->dimension, m = previous->components;
+    if (d < 2 || d > 3) throw InvalidArgument("m_step supports d = 2 or 3");
+    if (!(total_weight > 0.0)) throw RuntimeError("m_step: zero total weight");
+    auto x = stage_in(ctx, points, size_t(n) * d);
+    auto pw = stage_in(ctx, weights, size_t(n));
+    auto r = stage_in(ctx, resp, size_t(m) * n);
+    auto pmu = stage_in(ctx, previous->means, size_t(m) * d);
+    auto pcv = stage_in(ctx, previous->covariances, size_t(m) * d * d);
+    double* ow = arena<double>(ctx, m);
+    double* omu = arena<double>(ctx, size_t(m) * d);
+    double* ocv = arena<double>(ctx, size_t(m) * d * d);
+    int* dg = arena<int>(ctx, m);
+    int* bad = arena<int>(ctx, 1);
+    VDFCG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
+    launch_m_step(ctx, d, x.dev, pw.dev, n, total_weight, r.dev, m, pmu.dev, pcv.dev, ow, omu, ocv,
+                  dg, bad);
+    if (read_scalar(ctx, bad)) throw RuntimeError("m_step: invalid responsibility mass");
+    copy_out(ctx, out->weights, ow, m);
+    copy_out(ctx, out->means, omu, size_t(m) * d);
+    copy_out(ctx, out->covariances, ocv, size_t(m) * d * d);
+    std::vector<int> h(std::max(m, 1));
+    VDFCG_CUDA(cudaMemcpyAsync(h.data(), dg, sizeof(int) * m, cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    out->dimension = d;
+    out->components = m;
+    if (out->scale && out->offset && previous->scale && previous->offset)
+      for (int a = 0; a < d; ++a) {
+        out->scale[a] = previous->scale[a];
+        out->offset[a] = previous->offset[a];
+      }
+    int k = 0;
+    for (int i = 0; i < m; ++i)
+      if (h[i]) {
+        if (degenerate) degenerate[k] = i;
+        ++k;
+      }
+    if (n_degenerate) *n_degenerate = k;
+  });
+}
+
+int vdfcg_prune_one(vdfcg_ctx* ctx, vdfcg_model* model, double threshold, int32_t iteration,
+                    int32_t* pruned, int32_t* event_component, double* event_weight) {
+  (void)iteration;
+  return guard_impl([&] {
+    begin(ctx);
+    if (!model) throw InvalidArgument("null model");
+    const int d = model->dimension, m = model->components;
+    if (d < 1 || d > 3 || m < 0 || m > VDFCG_MAX_COMPONENTS) throw InvalidArgument("bad model");
+    double* w = arena<double>(ctx, VDFCG_MAX_COMPONENTS);
+    double* mu = arena<double>(ctx, VDFCG_MAX_COMPONENTS * 3);
+    double* cv = arena<double>(ctx, VDFCG_MAX_COMPONENTS * 9);
+    copy_out(ctx, w, model->weights, m);
+    copy_out(ctx, mu, model->means, size_t(m) * d);
+    copy_out(ctx, cv, model->covariances, size_t(m) * d * d);
+    int* mm = arena<int>(ctx, 4);
+    double* ew = arena<double>(ctx, 1);
+    VDFCG_CUDA(cudaMemcpyAsync(mm, &m, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    if (d == 1) throw InvalidArgument("prune_one supports d = 2 or 3");
+    launch_prune_one(ctx, d, w, mu, cv, mm, threshold, mm + 1, mm + 2, ew);
+    int hm[4];
+    double hw;
+    VDFCG_CUDA(cudaMemcpyAsync(hm, mm, sizeof(hm), cudaMemcpyDeviceToHost, ctx->stream));
+    VDFCG_CUDA(cudaMemcpyAsync(&hw, ew, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    copy_out(ctx, model->weights, w, hm[0]);
+    copy_out(ctx, model->means, mu, size_t(hm[0]) * d);
+    copy_out(ctx, model->covariances, cv, size_t(hm[0]) * d * d);
+    sync(ctx);
+    model->components = hm[0];
+    *pruned = hm[1];
+    if (hm[1]) {
+      *event_component = hm[2];
+      *event_weight = hw;
+    }
+  });
+}
+
+int vdfcg_repair_covariance(vdfcg_ctx* ctx, const double* sigma, int32_t d, double* out,
+                            int32_t* doublings) {
+  return guard_impl([&] {
+    begin(ctx);
+    if (d < 1 || d > 3) throw InvalidArgument("repair_covariance supports d <= 3");
+    auto s = stage_in(ctx, sigma, size_t(d) * d);
+    double* o = arena<double>(ctx, 9);
+    int* di = arena<int>(ctx, 2);
+    launch_repair(ctx, d, s.dev, o, di, di + 1);
+    int h[2];
+    VDFCG_CUDA(cudaMemcpyAsync(h, di, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    if (!h[1]) throw RepairFailed("covariance repair failed after 60 doublings");
+    copy_out(ctx, out, o, size_t(d) * d);
+    sync(ctx);
+    if (doublings) *doublings = h[0];
+  });
+}
+
+int vdfcg_fit(vdfcg_ctx* ctx, const double* points, const double* weights, int64_t n, int32_t d,
+              double total_weight, const vdfcg_fit_config* cfg, vdfcg_fit_result* res) {
+  return guard_impl([&] {
+    begin(ctx);
+    if (d != 2 && d != 3) throw InvalidArgument("dimension must be 2 or 3");
+    validate_config(cfg, d);
+    if (!res) throw InvalidArgument("null result");
+    const int K = std::max(cfg->initial_components, cfg->warm_start ? cfg->warm_start->components : 0);
+    if (res->capacity_components < K) throw InvalidArgument("result capacity_components too small");
+    if (res->capacity_trace < cfg->max_em_iterations)
+      throw InvalidArgument("result capacity_trace too small");
+    auto x = stage_in(ctx, points, size_t(n) * d);
+    auto w = stage_in(ctx, weights, size_t(n));
+    EmConfig e = make_em_config(ctx, cfg, d);
+    EmOut o = alloc_em_out(ctx, 1, d, K, cfg->max_em_iterations, true);
+    launch_em_points(ctx, d, x.dev, w.dev, n, total_weight, e, o);
+    int st[4];  // status, comps, iters, conv
+    VDFCG_CUDA(cudaMemcpyAsync(&st[0], o.status, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    VDFCG_CUDA(cudaMemcpyAsync(&st[1], o.comps, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    VDFCG_CUDA(cudaMemcpyAsync(&st[2], o.iters, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    VDFCG_CUDA(cudaMemcpyAsync(&st[3], o.conv, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    int ne = 0, eax = -1;
+    double ev = 0.0;
+    VDFCG_CUDA(cudaMemcpyAsync(&ne, o.n_events, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    VDFCG_CUDA(cudaMemcpyAsync(&eax, o.err_axis, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    VDFCG_CUDA(cudaMemcpyAsync(&ev, o.err_value, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    if (st[0]) throw_status(st[0], eax, ev, true);
+    const int M = st[1];
+    copy_out(ctx, res->model.weights, o.w, M);
+    copy_out(ctx, res->model.means, o.mu, size_t(M) * d);
+    copy_out(ctx, res->model.covariances, o.cov, size_t(M) * d * d);
+    copy_out(ctx, res->loglik_trace, o.trace, size_t(st[2]));
+    copy_out(ctx, res->event_iteration, o.ev_it, size_t(ne));
+    copy_out(ctx, res->event_component, o.ev_comp, size_t(ne));
+    copy_out(ctx, res->event_weight, o.ev_w, size_t(ne));
+    sync(ctx);
+    res->model.dimension = d;
+    res->model.components = M;
+    res->trace_len = st[2];
+    res->iterations_used = st[2];
+    res->converged = st[3];
+    res->n_events = ne;
+  });
+}
+
+// ------------------------------------------------------------------ writer
+int vdfcg_encode_model(vdfcg_ctx* ctx, const vdfcg_model* model, const vdfcg_model_meta* meta,
+                       uint8_t* out, int64_t capacity, int64_t* length) {
+  return guard_impl([&] {
+    begin(ctx);
+    if (!model || !meta || !length) throw InvalidArgument("null argument");
+    const int d = model->dimension, m = model->components;
+    if (d < 1) throw InvalidArgument("model dimension must be positive");
+    if (m < 1) throw InvalidArgument("model has no components");
+    if (d > 3) throw InvalidArgument("model dimension must be <= 3");
+    auto w = stage_in(ctx, model->weights, m);
+    auto mu = stage_in(ctx, model->means, size_t(m) * d);
+    auto cv = stage_in(ctx, model->covariances, size_t(m) * d * d);
+    int* code = arena<int>(ctx, 1);
+    VDFCG_LAUNCH(ctx, "validate_model", validate_model_kernel<<<1, 32, 0, ctx->stream>>>(d, m, w.dev, cv.dev, code));
+    const int c = read_scalar(ctx, code);
+    if (c == 2) throw InvalidArgument("component weight must be > 0");
+    if (c == 3) throw InvalidArgument("component covariance is not symmetric");
+    if (c == 4) throw InvalidArgument("component weights must sum to 1");
+    const bool map = model->scale && model->offset;
+    const double* pw = w.dev;
+    const double* pmu = mu.dev;
+    const double* pcv = cv.dev;
+    if (map) {
+      auto sc = stage_in(ctx, model->scale, d);
+      auto of = stage_in(ctx, model->offset, d);
+      double* ow = arena<double>(ctx, m);
+      double* omu = arena<double>(ctx, size_t(m) * d);
+      double* ocv = arena<double>(ctx, size_t(m) * d * d);
+      launch_canonicalize(ctx, d, m, w.dev, mu.dev, cv.dev, sc.dev, of.dev, ow, omu, ocv);
+      pw = ow;
+      pmu = omu;
+      pcv = ocv;
+    }
+    PackMeta pm = make_pack_meta(ctx, meta, d);
+    int32_t* comps = arena<int32_t>(ctx, 1);
+    VDFCG_CUDA(cudaMemcpyAsync(comps, &m, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    PackIn in{1, m, nullptr, comps, pw, pmu, pcv};
+    int64_t* offs = arena<int64_t>(ctx, 2);
+    const int64_t total = launch_pack_offsets(ctx, in, pm, offs);
+    if (total > capacity) throw InvalidArgument("encode_model: capacity too small");
+    uint8_t* buf = arena<uint8_t>(ctx, total);
+    launch_pack(ctx, in, pm, offs, buf);
+    copy_out(ctx, out, buf, size_t(total));
+    sync(ctx);
+    *length = total;
+  });
+}
+
+// ------------------------------------------------------------------ cells
+static CellBinsDev bins_dev(vdfcg_ctx* ctx, const CellsDev& c, vdfcg_cell_bins* out,
+                            std::vector<std::function<void()>>& fin) {
+  CellBinsDev b{};
+  const size_t nc = c.n_cells, n = size_t(c.n);
+  if (out && out->nnz) {
+    auto s1 = stage_out(ctx, out->nnz, nc);
+    auto s2 = stage_out(ctx, out->keys, n);
+    auto s3 = stage_out(ctx, out->counts, n);
+    auto s4 = stage_out(ctx, out->out_of_range, nc);
+    auto s5 = stage_out(ctx, out->in_range, nc);
+    b = {s1.dev, s2.dev, s3.dev, s4.dev, s5.dev};
+    fin.push_back([=] {
+      finish(ctx, s1);
+      finish(ctx, s2);
+      finish(ctx, s3);
+      finish(ctx, s4);
+      finish(ctx, s5);
+    });
+  } else {
+    b = {arena<int32_t>(ctx, nc), arena<uint32_t>(ctx, n), arena<double>(ctx, n),
+         arena<double>(ctx, nc), arena<double>(ctx, nc)};
+  }
+  return b;
+}
+
+static EmOut results_dev(vdfcg_ctx* ctx, int n_cells, int d, vdfcg_cell_results* r,
+                         std::vector<std::function<void()>>& fin) {
+  if (!r) throw InvalidArgument("null cell results");
+  const int K = r->capacity_components;
+  const size_t nc = n_cells;
+  EmOut o{};
+  o.K = K;
+  o.trace_cap = r->loglik_trace ? r->capacity_trace : 0;
+  auto st = stage_out(ctx, r->status, nc);
+  auto cm = stage_out(ctx, r->components, nc);
+  auto it = stage_out(ctx, r->iterations, nc);
+  auto cv = stage_out(ctx, r->converged, nc);
+  auto w = stage_out(ctx, r->weights, nc * K);
+  auto mu = stage_out(ctx, r->means, nc * K * d);
+  auto co = stage_out(ctx, r->covariances, nc * K * d * d);
+  auto fl = stage_out(ctx, r->final_loglik, nc);
+  auto tr = stage_out(ctx, r->loglik_trace, o.trace_cap ? nc * o.trace_cap : 0);
+  auto ne = stage_out(ctx, r->n_events, r->n_events ? nc : 0);
+  auto ei = stage_out(ctx, r->event_iteration, r->event_iteration ? nc * K : 0);
+  auto ec = stage_out(ctx, r->event_component, r->event_component ? nc * K : 0);
+  auto ew = stage_out(ctx, r->event_weight, r->event_weight ? nc * K : 0);
+  if (!st.dev || !cm.dev || !it.dev || !cv.dev || !w.dev || !mu.dev || !co.dev || !fl.dev)
+    throw InvalidArgument("cell results: status/components/iterations/converged/weights/means/"
+                          "covariances/final_loglik are required");
+  o.status = st.dev;
+  o.comps = cm.dev;
+  o.iters = it.dev;
+  o.conv = cv.dev;
+  o.w = w.dev;
+  o.mu = mu.dev;
+  o.cov = co.dev;
+  o.final_ll = fl.dev;
+  o.trace = tr.dev;
+  const bool ev = ne.dev && ei.dev && ec.dev && ew.dev;
+  o.n_events = ev ? ne.dev : nullptr;
+  o.ev_it = ev ? ei.dev : nullptr;
+  o.ev_comp = ev ? ec.dev : nullptr;
+  o.ev_w = ev ? ew.dev : nullptr;
+  o.err_axis = nullptr;
+  o.err_value = nullptr;
+  fin.push_back([=] {
+    finish(ctx, st);
+    finish(ctx, cm);
+    finish(ctx, it);
+    finish(ctx, cv);
+    finish(ctx, w);
+    finish(ctx, mu);
+    finish(ctx, co);
+    finish(ctx, fl);
+    finish(ctx, tr);
+    finish(ctx, ne);
+    finish(ctx, ei);
+    finish(ctx, ec);
+    finish(ctx, ew);
+  });
+  return o;
+}
+
+static bool any_host(const std::vector<std::function<void()>>& fin) { return !fin.empty(); }
+
+static void fit_cells_dev(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& b,
+                          const vdfcg_fit_config* cfg, const EmOut& o) {
+  if (o.K < std::max(cfg->initial_components, cfg->warm_start ? cfg->warm_start->components : 0))
+    throw InvalidArgument("cell results capacity_components too small");
+  if (o.trace_cap && o.trace_cap < cfg->max_em_iterations)
+    throw InvalidArgument("cell results capacity_trace too small");
+  EmConfig e = make_em_config(ctx, cfg, c.d);
+  KeyCells kc{};
+  kc.n_cells = c.n_cells;
+  kc.offsets = c.offsets;
+  kc.nnz = b.nnz;
+  kc.keys = b.keys;
+  kc.counts = b.counts;
+  kc.in_range = b.in_range;
+  kc.n_bins = c.n_bins;
+  for (int a = 0; a < 3; ++a) {
+    kc.lo[a] = c.lo[a];
+    kc.hi[a] = c.hi[a];
+  }
+  const double avg = c.n_cells ? double(c.n) / c.n_cells : 0.0;
+  launch_em_cells(ctx, c.d, kc, e, o, avg);
+}
+
+int vdfcg_bin_cells(vdfcg_ctx* ctx, const vdfcg_cells* cells, vdfcg_cell_bins* out) {
+  return guard_impl([&] {
+    begin(ctx);
+    CellsDev c = stage_cells(ctx, cells);
+    if (!out) throw InvalidArgument("null output");
+    std::vector<std::function<void()>> fin;
+    CellBinsDev b = bins_dev(ctx, c, out, fin);
+    launch_bin_cells(ctx, c, b);
+    for (auto& f : fin) f();
+    sync(ctx);
+  });
+}
+
+int vdfcg_fit_cells(vdfcg_ctx* ctx, const vdfcg_cells* cells, const vdfcg_cell_bins* bins,
+                    const vdfcg_fit_config* cfg, vdfcg_cell_results* out) {
+  return guard_impl([&] {
+    begin(ctx);
+    if (!cells || !bins) throw InvalidArgument("null argument");
+    validate_config(cfg, cells->dimension);
+    vdfcg_cells geom = *cells;
+    geom.weights = nullptr;
+    for (int a = 0; a < 3; ++a) geom.velocity[a] = nullptr;
+    if (geom.n_particles == 0) geom.velocity[0] = nullptr;
+    // geometry only: velocities are not read by the fitter
+    CellsDev c{};
+    c.d = cells->dimension;
+    if (c.d != 2 && c.d != 3) throw InvalidArgument("particle dimension must be 2 or 3");
+    c.n = cells->n_particles;
+    c.n_cells = cells->n_cells;
+    c.offsets = stage_in(ctx, cells->cell_offsets, size_t(c.n_cells) + 1).dev;
+    c.n_bins = cells->n_bins;
+    for (int a = 0; a < 3; ++a) {
+      c.lo[a] = cells->lo[a];
+      c.hi[a] = cells->hi[a];
+    }
+    CellBinsDev b{};
+    b.nnz = stage_in(ctx, bins->nnz, c.n_cells).dev;
+    b.keys = stage_in(ctx, bins->keys, size_t(c.n)).dev;
+    b.counts = stage_in(ctx, bins->counts, size_t(c.n)).dev;
+    b.in_range = stage_in(ctx, bins->in_range, c.n_cells).dev;
+    std::vector<std::function<void()>> fin;
+    EmOut o = results_dev(ctx, c.n_cells, c.d, out, fin);
+    fit_cells_dev(ctx, c, b, cfg, o);
+    for (auto& f : fin) f();
+    if (any_host(fin)) sync(ctx);
+  });
+}
+
+static PackIn pack_in_from(vdfcg_ctx* ctx, int n_cells, int d, const vdfcg_cell_results* r) {
+  const int K = r->capacity_components;
+  const size_t nc = n_cells;
+  PackIn in{};
+  in.n_cells = n_cells;
+  in.K = K;
+  in.status = stage_in(ctx, r->status, nc).dev;
+  in.comps = stage_in(ctx, r->components, nc).dev;
+  in.w = stage_in(ctx, r->weights, nc * K).dev;
+  in.mu = stage_in(ctx, r->means, nc * K * d).dev;
+  in.cov = stage_in(ctx, r->covariances, nc * K * d * d).dev;
+  return in;
+}
+
+int vdfcg_pack_cells(vdfcg_ctx* ctx, int32_t n_cells, int32_t d, const vdfcg_cell_results* res,
+                     const vdfcg_model_meta* meta, uint8_t* records, int64_t capacity,
+                     int64_t* record_offsets) {
+  return guard_impl([&] {
+    begin(ctx);
+    if (!res || !record_offsets) throw InvalidArgument("null argument");
+    if (d != 2 && d != 3) throw InvalidArgument("dimension must be 2 or 3");
+    PackIn in = pack_in_from(ctx, n_cells, d, res);
+    PackMeta pm = make_pack_meta(ctx, meta, d);
+    auto offs = stage_out(ctx, record_offsets, size_t(n_cells) + 1);
+    const int64_t total = launch_pack_offsets(ctx, in, pm, offs.dev);
+    if (total > capacity) throw InvalidArgument("pack_cells: capacity too small");
+    auto rec = stage_out(ctx, records, size_t(total));
+    if (total) launch_pack(ctx, in, pm, offs.dev, rec.dev);
+    finish(ctx, offs);
+    finish(ctx, rec);
+    sync(ctx);
+  });
+}
+
+int vdfcg_compress_cells(vdfcg_ctx* ctx, const vdfcg_cells* cells, const vdfcg_fit_config* cfg,
+                         vdfcg_cell_bins* bins, vdfcg_cell_results* out,
+                         const vdfcg_model_meta* meta, uint8_t* records, int64_t capacity,
+                         int64_t* record_offsets) {
+  return guard_impl([&] {
+    begin(ctx);
+    CellsDev c = stage_cells(ctx, cells);
+    validate_config(cfg, c.d);
+    std::vector<std::function<void()>> fin;
+    CellBinsDev b = bins_dev(ctx, c, bins, fin);
+    EmOut o = results_dev(ctx, c.n_cells, c.d, out, fin);
+    launch_bin_cells(ctx, c, b);
+    fit_cells_dev(ctx, c, b, cfg, o);
+    if (records || record_offsets) {
+      if (!meta || !record_offsets) throw InvalidArgument("packing needs meta and record_offsets");
+      PackIn in{c.n_cells, o.K, o.status, o.comps, o.w, o.mu, o.cov};
+      PackMeta pm = make_pack_meta(ctx, meta, c.d);
+      auto offs = stage_out(ctx, record_offsets, size_t(c.n_cells) + 1);
+      const int64_t total = launch_pack_offsets(ctx, in, pm, offs.dev);
+      if (total > capacity) throw InvalidArgument("compress_cells: record capacity too small");
+      auto rec = stage_out(ctx, records, size_t(total));
+      if (total) launch_pack(ctx, in, pm, offs.dev, rec.dev);
+      fin.push_back([=] {
+        finish(ctx, offs);
+        finish(ctx, rec);
+      });
+    }
+    for (auto& f : fin) f();
+    if (any_host(fin)) sync(ctx);
+  });
+}
+
+int vdfcg_synth_cells(vdfcg_ctx* ctx, int32_t d, int32_t n_cells, const int64_t* cell_offsets,
+                      uint64_t seed, int32_t species, double* u, double* v, double* w) {
+  return guard_impl([&] {
+    begin(ctx);
+    if (d != 2 && d != 3) throw InvalidArgument("dimension must be 2 or 3");
+    if (!is_device_pointer(cell_offsets) || !is_device_pointer(u) || !is_device_pointer(v) ||
+        (d == 3 && !is_device_pointer(w)))
+      throw InvalidArgument("vdfcg_synth_cells takes device pointers");
+    if (n_cells > 0) launch_synth(ctx, d, n_cells, cell_offsets, seed, species, u, v, w);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,81 @@
+// common.cuh — shared device helpers for the vdfcg kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+
+#define VDFCG_DEV __device__ __forceinline__
+#define VDFCG_HD __host__ __device__ __forceinline__
+
+namespace vdfcg {
+
+constexpr int kWarp = 32;
+constexpr int kMaxK = 16;   // VDFCG_MAX_COMPONENTS
+constexpr int kMaxWarps = 32;
+
+// log(2*pi) as a double (the reference computes std::log(2.0 * M_PI), gaussian.hpp:31).
+constexpr double kLog2Pi = 1.8378770664093453;
+constexpr double kMassFloorRel = 1e-250;  // wgmm.cpp:20
+
+VDFCG_DEV double dinf() { return __longlong_as_double(0x7ff0000000000000ULL); }
+VDFCG_DEV double dnan() { return __longlong_as_double(0x7ff8000000000000ULL); }
+
+// histogram.cpp:36-41 bin_index. Left-closed right-open, top edge closed. NaN is out of
+// range (the reference's x86 float->int conversion of floor(NaN) yields INT_MIN, which
+// fails the range test at histogram.cpp:70). (v - lo) * inv cannot contract into an FMA.
+VDFCG_DEV int bin_index(double v, double lo, double hi, int n, double inv) {
+  if (!(v >= lo && v <= hi)) return -1;
+  int i = static_cast<int>(floor((v - lo) * inv));
+  if (i >= n) i = n - 1;
+  return i;
+}
+
+// GridSpec::center_x (types.hpp:48,51): lo + (i + 0.5) * ((hi - lo) / n), no FMA.
+VDFCG_DEV double bin_center(double lo, double hi, int n, int i) {
+  const double dx = (hi - lo) / static_cast<double>(n);
+  return __dadd_rn(lo, __dmul_rn(static_cast<double>(i) + 0.5, dx));
+}
+
+template <class T>
+VDFCG_DEV T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <class T>
+VDFCG_DEV T warp_min(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    T u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = u < v ? u : v;
+  }
+  return v;
+}
+
+template <class T>
+VDFCG_DEV T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    T u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = u > v ? u : v;
+  }
+  return v;
+}
+
+// Kahan accumulator (gaussian.hpp:55-68). Explicit _rn intrinsics keep the
+// compensation exact regardless of contraction.
+struct Kahan {
+  double s = 0.0, c = 0.0;
+  VDFCG_DEV void add(double x) {
+    const double y = __dsub_rn(x, c);
+    const double t = __dadd_rn(s, y);
+    c = __dsub_rn(__dsub_rn(t, s), y);
+    s = t;
+  }
+  VDFCG_DEV double value() const { return __dsub_rn(s, c); }
+};
+
+}  // namespace vdfcg

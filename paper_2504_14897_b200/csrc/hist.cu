@@ -1,0 +1,726 @@
+// hist.cu — velocity histogram kernels (sm_100a).
+//
+// K1 hist2d: bin_particles / all_planes (histogram.cpp:45-84). One pass over the
+//    particle columns (all three marginals from one read for all_planes), per-CTA
+//    shared-memory privatised u32 counters (unit weights: exact integers) merged into
+//    global memory with one atomic per non-empty bin, out-of-range mass per CTA.
+// K2 cells_dense: per-cell bins^d histograms for cells much larger than the grid
+//    (SURVEY.md App. A), work items = (cell, chunk), shared-memory privatised counters.
+// K3 cells_sort: per-cell sort of composite (bin, particle) keys for cells much
+//    smaller than the grid (48^3, 64^3): the sorted runs ARE the compacted histogram in
+//    ascending bin order (= to_weighted_points(drop_empty) order), and fractional
+//    weights are summed in particle order, i.e. bit-identical to the reference's
+//    sequential `counts(i,j) += w` (histogram.cpp:70-73).
+// K4 compaction of dense grids (histogram.cpp:86-109 order: i outer, j, k inner).
+#include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "hist.cuh"
+
+namespace vdfcg {
+
+// ---------------------------------------------------------------------------- K1
+struct Hist2dParams {
+  int ax[3], ay[3];
+  int n_bins;
+  double xlo[3], xhi[3], ylo[3], yhi[3], invx[3], invy[3];
+};
+
+template <int NP, bool W, bool SMEM>
+__global__ void __launch_bounds__(512) hist2d_kernel(const double* __restrict__ vel, int64_t n,
+                                                     const double* __restrict__ w, Hist2dParams p,
+                                                     unsigned* __restrict__ gcnt,
+                                                     double* __restrict__ gcntw,
+                                                     unsigned long long* __restrict__ goor,
+                                                     double* __restrict__ goorw, int* err) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int nb = p.n_bins;
+  const int nn = nb * nb;
+  unsigned* sh = reinterpret_cast<unsigned*>(smem_raw);
+  double* shw = reinterpret_cast<double*>(smem_raw);
+  if (SMEM) {
+    for (int f = threadIdx.x; f < NP * nn; f += blockDim.x) {
+      if (W) shw[f] = 0.0; else sh[f] = 0u;
+    }
+    __syncthreads();
+  }
+  unsigned long long oor[NP];
+  double oorw[NP];
+#pragma unroll
+  for (int q = 0; q < NP; ++q) {
+    oor[q] = 0;
+    oorw[q] = 0.0;
+  }
+  bool bad = false;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double wt = 1.0;
+    if (W) {
+      wt = __ldg(w + i);
+      bad |= !(wt > 0.0);
+    }
+    // Load each needed axis once (all_planes: u, v, w read once for three planes).
+    double v[3];
+    int idx[3][2];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) v[a] = 0.0;
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const double vx = __ldg(vel + static_cast<int64_t>(p.ax[q]) * n + i);
+      const double vy = __ldg(vel + static_cast<int64_t>(p.ay[q]) * n + i);
+      idx[q][0] = bin_index(vx, p.xlo[q], p.xhi[q], nb, p.invx[q]);
+      idx[q][1] = bin_index(vy, p.ylo[q], p.yhi[q], nb, p.invy[q]);
+    }
+    (void)v;
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const int bi = idx[q][0], bj = idx[q][1];
+      if (bi < 0 || bj < 0) {
+        if (W) oorw[q] += wt; else oor[q] += 1;
+      } else {
+        const int f = q * nn + bi + bj * nb;  // column-major counts(i, j)
+        if (SMEM) {
+          if (W) atomicAdd(shw + f, wt); else atomicAdd(sh + f, 1u);
+        } else {
+          if (W) atomicAdd(gcntw + f, wt); else atomicAdd(gcnt + f, 1u);
+        }
+      }
+    }
+  }
+  if (W && bad) atomicOr(err, 1);
+  if (SMEM) {
+    __syncthreads();
+    for (int f = threadIdx.x; f < NP * nn; f += blockDim.x) {
+      if (W) {
+        const double c = shw[f];
+        if (c != 0.0) atomicAdd(gcntw + f, c);
+      } else {
+        const unsigned c = sh[f];
+        if (c) atomicAdd(gcnt + f, c);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NP; ++q) {
+    if (W) {
+      const double s = warp_sum(oorw[q]);
+      if ((threadIdx.x & 31) == 0 && s != 0.0) atomicAdd(goorw + q, s);
+    } else {
+      const unsigned long long s = warp_sum(oor[q]);
+      if ((threadIdx.x & 31) == 0 && s) atomicAdd(goor + q, s);
+    }
+  }
+}
+
+__global__ void u32_to_f64_kernel(const unsigned* __restrict__ in, double* __restrict__ out,
+                                  int64_t n) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<double>(in[i]);
+}
+
+__global__ void u64_to_f64_kernel(const unsigned long long* in, double* out, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = static_cast<double>(in[i]);
+}
+
+template <int NP, bool W, bool SMEM>
+static void hist2d_dispatch(vdfcg_ctx* ctx, int grid, int block, size_t smem, const double* vel,
+                            int64_t n, const double* w, const Hist2dParams& p, unsigned* gcnt,
+                            double* gcntw, unsigned long long* goor, double* goorw, int* err) {
+  auto k = hist2d_kernel<NP, W, SMEM>;
+  if (smem > 48 * 1024)
+    VDFCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+  VDFCG_LAUNCH(ctx, "hist2d", k<<<grid, block, smem, ctx->stream>>>(vel, n, w, p, gcnt, gcntw,
+                                                                     goor, goorw, err));
+}
+
+void launch_hist2d(vdfcg_ctx* ctx, const double* vel, int64_t n, int d, const double* w,
+                   int nplanes, const int* ax, const int* ay, int n_bins, const double* xlo,
+                   const double* xhi, const double* ylo, const double* yhi, double* counts_out,
+                   double* oor_out) {
+  (void)d;
+  Hist2dParams p{};
+  p.n_bins = n_bins;
+  for (int q = 0; q < nplanes; ++q) {
+    p.ax[q] = ax[q];
+    p.ay[q] = ay[q];
+    p.xlo[q] = xlo[q];
+    p.xhi[q] = xhi[q];
+    p.ylo[q] = ylo[q];
+    p.yhi[q] = yhi[q];
+    p.invx[q] = n_bins / (xhi[q] - xlo[q]);  // histogram.cpp:64-65
+    p.invy[q] = n_bins / (yhi[q] - ylo[q]);
+  }
+  const int64_t nn = static_cast<int64_t>(n_bins) * n_bins * nplanes;
+  const bool weighted = w != nullptr;
+  const size_t elem = weighted ? 8 : 4;
+  const size_t smem = static_cast<size_t>(nn) * elem;
+  const bool use_smem = smem <= 112 * 1024;
+  int* err = arena<int>(ctx, 1);
+  VDFCG_CUDA(cudaMemsetAsync(err, 0, sizeof(int), ctx->stream));
+  unsigned* gcnt = nullptr;
+  unsigned long long* goor = nullptr;
+  if (weighted) {
+    VDFCG_CUDA(cudaMemsetAsync(counts_out, 0, nn * sizeof(double), ctx->stream));
+    VDFCG_CUDA(cudaMemsetAsync(oor_out, 0, nplanes * sizeof(double), ctx->stream));
+  } else {
+    gcnt = arena<unsigned>(ctx, nn);
+    goor = arena<unsigned long long>(ctx, nplanes);
+    VDFCG_CUDA(cudaMemsetAsync(gcnt, 0, nn * sizeof(unsigned), ctx->stream));
+    VDFCG_CUDA(cudaMemsetAsync(goor, 0, nplanes * sizeof(unsigned long long), ctx->stream));
+  }
+  const int block = 512;
+  int per_sm = 1;
+  if (use_smem) per_sm = std::max(1, std::min(4, static_cast<int>((200 * 1024) / std::max<size_t>(smem, 1))));
+  else per_sm = 4;
+  int64_t want = (n + block - 1) / block;
+  int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(ctx->sm_count) * per_sm)));
+  const size_t sm = use_smem ? smem : 0;
+#define VDFCG_H2D(NP)                                                                         \
+  if (weighted) {                                                                             \
+    if (use_smem) hist2d_dispatch<NP, true, true>(ctx, grid, block, sm, vel, n, w, p, gcnt,   \
+                                                  counts_out, goor, oor_out, err);            \
+    else hist2d_dispatch<NP, true, false>(ctx, grid, block, sm, vel, n, w, p, gcnt,           \
+                                          counts_out, goor, oor_out, err);                    \
+  } else {                                                                                    \
+    if (use_smem) hist2d_dispatch<NP, false, true>(ctx, grid, block, sm, vel, n, w, p, gcnt,  \
+                                                   counts_out, goor, oor_out, err);           \
+    else hist2d_dispatch<NP, false, false>(ctx, grid, block, sm, vel, n, w, p, gcnt,          \
+                                           counts_out, goor, oor_out, err);                   \
+  }
+  if (n > 0) {
+    if (nplanes == 1) {
+      VDFCG_H2D(1)
+    } else {
+      VDFCG_H2D(3)
+    }
+  }
+#undef VDFCG_H2D
+  if (!weighted) {
+    const int g2 = static_cast<int>(std::min<int64_t>((nn + 255) / 256, ctx->sm_count * 8));
+    VDFCG_LAUNCH(ctx, "hist2d_finalize",
+                 u32_to_f64_kernel<<<std::max(g2, 1), 256, 0, ctx->stream>>>(gcnt, counts_out, nn));
+    VDFCG_LAUNCH(ctx, "hist2d_finalize",
+                 u64_to_f64_kernel<<<1, 32, 0, ctx->stream>>>(goor, oor_out, nplanes));
+  }
+  if (weighted) {
+    int* h = static_cast<int*>(ctx->pinned);
+    VDFCG_CUDA(cudaMemcpyAsync(h, err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    if (*h) throw InvalidArgument("particle weights must all be > 0");
+  }
+}
+
+// ------------------------------------------------------- to_weighted_points (2D)
+__global__ void __launch_bounds__(1024) twp_kernel(const double* __restrict__ counts, int nb,
+                                                   double xlo, double xhi, double ylo,
+                                                   double yhi, int drop_empty, int64_t capacity,
+                                                   double* __restrict__ points,
+                                                   double* __restrict__ weights,
+                                                   int64_t* count_out, double* total_out) {
+  using Reduce = cub::BlockReduce<long long, 1024>;
+  using Scan = cub::BlockScan<int, 1024>;
+  __shared__ typename Reduce::TempStorage rs;
+  __shared__ typename Scan::TempStorage ss;
+  __shared__ long long s_kept;
+  __shared__ int s_run;
+  const int64_t nn = static_cast<int64_t>(nb) * nb;
+  // Pass 1: count kept bins; in-range total summed in column-major storage order by
+  // one thread (Histogram2D::in_range_count, histogram.hpp:25).
+  long long kept = 0;
+  for (int64_t f = threadIdx.x; f < nn; f += blockDim.x) kept += (counts[f] > 0.0) ? 1 : 0;
+  long long tot_kept = Reduce(rs).Sum(kept);
+  if (threadIdx.x == 0) {
+    s_kept = drop_empty ? tot_kept : nn;
+    double t = 0.0;
+    for (int64_t f = 0; f < nn; ++f) t += counts[f];
+    *total_out = t;
+    *count_out = s_kept;
+    s_run = 0;
+  }
+  __syncthreads();
+  const int64_t ld = s_kept;
+  if (ld > capacity) return;
+  // Pass 2: i outer, j inner (histogram.cpp:97-106), ordered compaction per tile.
+  for (int64_t base = 0; base < nn; base += blockDim.x) {
+    const int64_t f = base + threadIdx.x;  // f = i*nb + j
+    double c = 0.0;
+    int keep = 0;
+    int i = 0, j = 0;
+    if (f < nn) {
+      i = static_cast<int>(f / nb);
+      j = static_cast<int>(f % nb);
+      c = counts[i + static_cast<int64_t>(j) * nb];
+      keep = (!drop_empty || c > 0.0) ? 1 : 0;
+    }
+    int pos, total;
+    Scan(ss).ExclusiveSum(keep, pos, total);
+    const int r = s_run + pos;
+    if (keep) {
+      points[r] = bin_center(xlo, xhi, nb, i);
+      points[ld + r] = bin_center(ylo, yhi, nb, j);
+      weights[r] = c;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_run += total;
+    __syncthreads();
+  }
+}
+
+int64_t launch_to_weighted_points(vdfcg_ctx* ctx, const double* counts, int n_bins, double xlo,
+                                  double xhi, double ylo, double yhi, bool drop_empty,
+                                  int64_t capacity, double* points, double* weights,
+                                  double* total_weight_dev) {
+  int64_t* cnt = arena<int64_t>(ctx, 1);
+  VDFCG_LAUNCH(ctx, "to_weighted_points",
+               twp_kernel<<<1, 1024, 0, ctx->stream>>>(counts, n_bins, xlo, xhi, ylo, yhi,
+                                                       drop_empty ? 1 : 0, capacity, points,
+                                                       weights, cnt, total_weight_dev));
+  int64_t* h = static_cast<int64_t*>(ctx->pinned);
+  VDFCG_CUDA(cudaMemcpyAsync(h, cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  return *h;
+}
+
+// ---------------------------------------------------------------------- cells
+struct CellGeom {
+  int n_bins;
+  double lo[3], hi[3], inv[3];
+};
+
+template <int D>
+VDFCG_DEV int64_t cell_key(const double* const* vel, int64_t i, const CellGeom& g) {
+  int64_t key = 0;
+  bool out = false;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    const int b = bin_index(__ldg(vel[a] + i), g.lo[a], g.hi[a], g.n_bins, g.inv[a]);
+    out |= b < 0;
+    key = key * g.n_bins + b;
+  }
+  return out ? -1 : key;
+}
+
+struct VelPtrs {
+  const double* v[3];
+};
+
+// K2: work item = (cell, chunk of `chunk` particles).
+template <int D, bool SMEM>
+__global__ void __launch_bounds__(1024) cells_dense_kernel(
+    VelPtrs vp, const double* __restrict__ w, const int64_t* __restrict__ offsets, int n_cells,
+    const int64_t* __restrict__ item_off, int64_t chunk, CellGeom g, int64_t bins,
+    unsigned* __restrict__ dense, double* __restrict__ densew,
+    unsigned long long* __restrict__ oor_cnt, double* __restrict__ oorw, int* err) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned* sh = reinterpret_cast<unsigned*>(smem_raw);
+  const int64_t n_items = item_off[n_cells];
+  const bool weighted = w != nullptr;
+  for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+    // cell = last c with item_off[c] <= item
+    int lo = 0, hi = n_cells - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (item_off[mid] <= item) lo = mid; else hi = mid - 1;
+    }
+    const int c = lo;
+    const int64_t k = item - item_off[c];
+    const int64_t b = offsets[c] + k * chunk;
+    const int64_t e = min(offsets[c + 1], b + chunk);
+    if (SMEM) {
+      for (int64_t f = threadIdx.x; f < bins; f += blockDim.x) sh[f] = 0u;
+      __syncthreads();
+    }
+    unsigned long long oor = 0;
+    double ow = 0.0;
+    bool bad = false;
+    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+      const int64_t key = cell_key<D>(vp.v, i, g);
+      if (weighted) {
+        const double wt = __ldg(w + i);
+        bad |= !(wt > 0.0);
+        if (key < 0) ow += wt;
+        else atomicAdd(densew + static_cast<int64_t>(c) * bins + key, wt);
+      } else {
+        if (key < 0) ++oor;
+        else if (SMEM) atomicAdd(sh + key, 1u);
+        else atomicAdd(dense + static_cast<int64_t>(c) * bins + key, 1u);
+      }
+    }
+    if (bad) atomicOr(err, 1);
+    if (SMEM) {
+      __syncthreads();
+      for (int64_t f = threadIdx.x; f < bins; f += blockDim.x) {
+        const unsigned v = sh[f];
+        if (v) atomicAdd(dense + static_cast<int64_t>(c) * bins + f, v);
+      }
+      __syncthreads();
+    }
+    if (weighted) {
+      const double s = warp_sum(ow);
+      if ((threadIdx.x & 31) == 0 && s != 0.0) atomicAdd(oorw + c, s);
+    } else {
+      const unsigned long long s = warp_sum(oor);
+      if ((threadIdx.x & 31) == 0 && s) atomicAdd(oor_cnt + c, s);
+    }
+  }
+}
+
+// K4: ordered compaction of dense per-cell grids into the cell's CSR region.
+template <bool W>
+__global__ void __launch_bounds__(512) cells_compact_kernel(
+    int n_cells, int64_t bins, const unsigned* __restrict__ dense,
+    const double* __restrict__ densew, const unsigned long long* __restrict__ oor_cnt,
+    const double* __restrict__ oorw, const int64_t* __restrict__ offsets, int32_t* nnz,
+    uint32_t* __restrict__ keys, double* __restrict__ counts, double* oor_out, double* in_range) {
+  using Scan = cub::BlockScan<int, 512>;
+  using Reduce = cub::BlockReduce<unsigned long long, 512>;
+  using ReduceD = cub::BlockReduce<double, 512>;
+  __shared__ typename Scan::TempStorage ss;
+  __shared__ typename Reduce::TempStorage rs;
+  __shared__ typename ReduceD::TempStorage rds;
+  __shared__ int64_t s_run;
+  for (int c = blockIdx.x; c < n_cells; c += gridDim.x) {
+    const int64_t base = offsets[c];
+    const int64_t cap = offsets[c + 1] - base;
+    if (threadIdx.x == 0) s_run = 0;
+    __syncthreads();
+    unsigned long long tot = 0;
+    double totw = 0.0;
+    for (int64_t t0 = 0; t0 < bins; t0 += blockDim.x) {
+      const int64_t f = t0 + threadIdx.x;
+      unsigned v = 0;
+      double vw = 0.0;
+      if (f < bins) {
+        if (W) vw = densew[static_cast<int64_t>(c) * bins + f];
+        else v = dense[static_cast<int64_t>(c) * bins + f];
+      }
+      const int keep = W ? (vw > 0.0) : (v > 0u);
+      tot += v;
+      totw += vw;
+      int pos, total;
+      Scan(ss).ExclusiveSum(keep, pos, total);
+      const int64_t r = s_run + pos;
+      if (keep && r < cap) {
+        keys[base + r] = static_cast<uint32_t>(f);
+        counts[base + r] = W ? vw : static_cast<double>(v);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) s_run += total;
+      __syncthreads();
+    }
+    const unsigned long long t = Reduce(rs).Sum(tot);
+    __syncthreads();
+    const double tw = ReduceD(rds).Sum(totw);
+    if (threadIdx.x == 0) {
+      nnz[c] = static_cast<int32_t>(s_run);
+      oor_out[c] = W ? oorw[c] : static_cast<double>(oor_cnt[c]);
+      in_range[c] = W ? tw : static_cast<double>(t);
+    }
+    __syncthreads();
+  }
+}
+
+// K3: per-cell composite-key sort. key = (bin << IDXB) | local index; OOR bin = SENT.
+template <int D, int BLOCK, int IPT, bool W>
+__global__ void __launch_bounds__(BLOCK) cells_sort_kernel(
+    VelPtrs vp, const double* __restrict__ w, const int64_t* __restrict__ offsets, int n_cells,
+    CellGeom g, int binbits, int idxbits, int32_t* nnz, uint32_t* __restrict__ keys_out,
+    double* __restrict__ counts_out, double* oor_out, double* in_range, int* err) {
+  constexpr int CAP = BLOCK * IPT;
+  using Sort = cub::BlockRadixSort<uint32_t, BLOCK, IPT>;
+  using Scan = cub::BlockScan<int, BLOCK>;
+  using ReduceD = cub::BlockReduce<double, BLOCK>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  auto& sort_ts = *reinterpret_cast<typename Sort::TempStorage*>(smem_raw);
+  uint32_t* sk = reinterpret_cast<uint32_t*>(smem_raw);  // reused after the sort
+  uint32_t* pos = sk + CAP;                               // run heads [CAP + 1]
+  __shared__ typename Scan::TempStorage ss;
+  __shared__ typename ReduceD::TempStorage rds;
+  __shared__ int s_valid, s_nnz;
+  const uint32_t sent = (binbits >= 32) ? 0xffffffffu : ((1u << binbits) - 1u);
+  const uint32_t idxmask = (1u << idxbits) - 1u;
+  for (int c = blockIdx.x; c < n_cells; c += gridDim.x) {
+    const int64_t b = offsets[c];
+    const int nc = static_cast<int>(offsets[c + 1] - b);
+    uint32_t k[IPT];
+    bool bad = false;
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const int li = i * BLOCK + threadIdx.x;  // striped, coalesced loads
+      if (li < nc) {
+        const int64_t key = cell_key<D>(vp.v, b + li, g);
+        const uint32_t bin = key < 0 ? sent : static_cast<uint32_t>(key);
+        k[i] = (bin << idxbits) | static_cast<uint32_t>(li);
+        if (W) bad |= !(__ldg(w + b + li) > 0.0);
+      } else {
+        k[i] = 0xffffffffu;
+      }
+    }
+    if (W && bad) atomicOr(err, 1);
+    __syncthreads();
+    Sort(sort_ts).Sort(k, 0, binbits + idxbits);
+    __syncthreads();
+    // blocked arrangement: thread t holds sorted positions t*IPT + i
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) sk[threadIdx.x * IPT + i] = k[i];
+    __syncthreads();
+    int heads = 0, valid = 0;
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const int p = threadIdx.x * IPT + i;
+      if (p < nc) {
+        const uint32_t bin = sk[p] >> idxbits;
+        if (bin != sent) {
+          ++valid;
+          if (p == 0 || (sk[p - 1] >> idxbits) != bin) ++heads;
+        }
+      }
+    }
+    int hpos, htot;
+    Scan(ss).ExclusiveSum(heads, hpos, htot);
+    int vtot = 0;
+    {
+      __syncthreads();
+      int vp2;
+      Scan(ss).ExclusiveSum(valid, vp2, vtot);
+    }
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const int p = threadIdx.x * IPT + i;
+      if (p < nc) {
+        const uint32_t bin = sk[p] >> idxbits;
+        if (bin != sent && (p == 0 || (sk[p - 1] >> idxbits) != bin)) pos[hpos++] = p;
+      }
+    }
+    if (threadIdx.x == 0) {
+      s_nnz = htot;
+      s_valid = vtot;
+      pos[htot] = vtot;
+    }
+    __syncthreads();
+    const int nz = s_nnz;
+    double part = 0.0;
+    for (int r = threadIdx.x; r < nz; r += BLOCK) {
+      const int p0 = pos[r], p1 = pos[r + 1];
+      double v;
+      if (W) {
+        v = 0.0;  // particle order within the run: exact reference summation
+        for (int p = p0; p < p1; ++p) v += __ldg(w + b + (sk[p] & idxmask));
+      } else {
+        v = static_cast<double>(p1 - p0);
+      }
+      keys_out[b + r] = sk[p0] >> idxbits;
+      counts_out[b + r] = v;
+      part += v;
+    }
+    double tw = 0.0;
+    if (W) tw = ReduceD(rds).Sum(part);
+    if (threadIdx.x == 0) {
+      nnz[c] = nz;
+      if (W) {
+        double o = 0.0;
+        for (int p = s_valid; p < nc; ++p) o += __ldg(w + b + (sk[p] & idxmask));
+        oor_out[c] = o;
+        in_range[c] = tw;
+      } else {
+        oor_out[c] = static_cast<double>(nc - s_valid);
+        in_range[c] = static_cast<double>(s_valid);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void chunks_per_cell_kernel(const int64_t* offsets, int n_cells, int64_t chunk,
+                                       int64_t* out) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n_cells; c += gridDim.x * blockDim.x) {
+    const int64_t nc = offsets[c + 1] - offsets[c];
+    out[c] = (nc + chunk - 1) / chunk;
+  }
+}
+
+__global__ void __launch_bounds__(1024) scan_i64_kernel(const int64_t* in, int64_t* out, int64_t n) {
+  using Scan = cub::BlockScan<long long, 1024>;
+  __shared__ typename Scan::TempStorage ss;
+  const int64_t seg = (n + 1023) / 1024;
+  const int64_t s = threadIdx.x * seg, e = min(n, s + seg);
+  long long local = 0;
+  for (int64_t i = s; i < e; ++i) local += in[i];
+  long long pre, tot;
+  Scan(ss).ExclusiveSum(local, pre, tot);
+  for (int64_t i = s; i < e; ++i) {
+    const long long v = in[i];
+    out[i] = pre;
+    pre += v;
+  }
+  if (threadIdx.x == 0) out[n] = tot;
+}
+
+void launch_scan_i64(vdfcg_ctx* ctx, const int64_t* in, int64_t* out, int64_t n) {
+  VDFCG_LAUNCH(ctx, "scan", scan_i64_kernel<<<1, 1024, 0, ctx->stream>>>(in, out, n));
+}
+
+__global__ void max_cell_kernel(const int64_t* offsets, int n_cells, unsigned long long* out) {
+  unsigned long long m = 0;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n_cells; c += gridDim.x * blockDim.x)
+    m = max(m, static_cast<unsigned long long>(offsets[c + 1] - offsets[c]));
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+int64_t max_cell_size(vdfcg_ctx* ctx, const int64_t* offsets, int n_cells) {
+  unsigned long long* d = arena<unsigned long long>(ctx, 1);
+  VDFCG_CUDA(cudaMemsetAsync(d, 0, 8, ctx->stream));
+  const int grid = std::max(1, std::min((n_cells + 255) / 256, ctx->sm_count * 4));
+  VDFCG_LAUNCH(ctx, "max_cell", max_cell_kernel<<<grid, 256, 0, ctx->stream>>>(offsets, n_cells, d));
+  auto* h = static_cast<unsigned long long*>(ctx->pinned);
+  VDFCG_CUDA(cudaMemcpyAsync(h, d, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  return static_cast<int64_t>(*h);
+}
+
+static int bits_for(uint64_t v) {  // smallest b with 2^b > v
+  int b = 0;
+  while (b < 64 && (uint64_t(1) << b) <= v) ++b;
+  return b;
+}
+
+template <int D, int BLOCK, int IPT, bool W>
+static void launch_sort(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& out,
+                        const CellGeom& g, int binbits, int* err) {
+  using Sort = cub::BlockRadixSort<uint32_t, BLOCK, IPT>;
+  constexpr int CAP = BLOCK * IPT;
+  const size_t smem = std::max(sizeof(typename Sort::TempStorage), size_t(2 * CAP + 2) * 4);
+  auto k = cells_sort_kernel<D, BLOCK, IPT, W>;
+  VDFCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int occ = 0;
+  VDFCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, BLOCK, smem));
+  const int grid = std::max(1, std::min(c.n_cells, ctx->sm_count * std::max(occ, 1)));
+  int idxbits = bits_for(CAP - 1);
+  VelPtrs vp{{c.vel[0], c.vel[1], c.vel[2]}};
+  VDFCG_LAUNCH(ctx, "cells_sort",
+               k<<<grid, BLOCK, smem, ctx->stream>>>(vp, c.w, c.offsets, c.n_cells, g, binbits,
+                                                     idxbits, out.nnz, out.keys, out.counts,
+                                                     out.oor, out.in_range, err));
+}
+
+template <int D, bool W>
+static bool try_sort_path(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& out,
+                          const CellGeom& g, int binbits, int64_t maxc, int* err) {
+  auto fits = [&](int cap) { return maxc <= cap && binbits + bits_for(cap - 1) <= 32; };
+  if (fits(1024)) launch_sort<D, 128, 8, W>(ctx, c, out, g, binbits, err);
+  else if (fits(2048)) launch_sort<D, 256, 8, W>(ctx, c, out, g, binbits, err);
+  else if (fits(4096)) launch_sort<D, 256, 16, W>(ctx, c, out, g, binbits, err);
+  else if (fits(8192)) launch_sort<D, 512, 16, W>(ctx, c, out, g, binbits, err);
+  else return false;
+  return true;
+}
+
+template <int D>
+static void bin_cells_d(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& out) {
+  CellGeom g{};
+  g.n_bins = c.n_bins;
+  int64_t bins = 1;
+  for (int a = 0; a < D; ++a) {
+    g.lo[a] = c.lo[a];
+    g.hi[a] = c.hi[a];
+    g.inv[a] = c.n_bins / (c.hi[a] - c.lo[a]);
+    bins *= c.n_bins;
+  }
+  const bool weighted = c.w != nullptr;
+  int* err = arena<int>(ctx, 1);
+  VDFCG_CUDA(cudaMemsetAsync(err, 0, sizeof(int), ctx->stream));
+  const int64_t maxc = max_cell_size(ctx, c.offsets, c.n_cells);
+  const double avg = c.n_cells ? double(c.n) / c.n_cells : 0.0;
+  const int binbits = bits_for(static_cast<uint64_t>(bins));  // SENT = 2^binbits - 1 > any bin
+  // Sparse cells (or fractional weights, which the sort path sums bit-exactly): sort.
+  bool done = false;
+  if (maxc <= 8192 && (weighted || avg * 4.0 < double(bins) || maxc <= 1024)) {
+    done = weighted ? try_sort_path<D, true>(ctx, c, out, g, binbits, maxc, err)
+                    : try_sort_path<D, false>(ctx, c, out, g, binbits, maxc, err);
+  }
+  if (!done) {
+    // Dense per-cell grids (global scratch), shared-memory privatised when they fit.
+    unsigned* dense = nullptr;
+    double* densew = nullptr;
+    unsigned long long* oor_cnt = nullptr;
+    double* oorw = nullptr;
+    const int64_t total_bins = bins * c.n_cells;
+    if (weighted) {
+      densew = arena<double>(ctx, total_bins);
+      oorw = arena<double>(ctx, c.n_cells);
+      VDFCG_CUDA(cudaMemsetAsync(densew, 0, total_bins * 8, ctx->stream));
+      VDFCG_CUDA(cudaMemsetAsync(oorw, 0, c.n_cells * 8, ctx->stream));
+    } else {
+      dense = arena<unsigned>(ctx, total_bins);
+      oor_cnt = arena<unsigned long long>(ctx, c.n_cells);
+      VDFCG_CUDA(cudaMemsetAsync(dense, 0, total_bins * 4, ctx->stream));
+      VDFCG_CUDA(cudaMemsetAsync(oor_cnt, 0, c.n_cells * 8, ctx->stream));
+    }
+    const bool smem_ok = !weighted && bins * 4 <= 160 * 1024;
+    const int block = 1024;
+    // chunk: enough items to fill every SM several times, >= 16K particles each
+    int64_t chunk = std::max<int64_t>(16384, (c.n + int64_t(ctx->sm_count) * 4 - 1) /
+                                                 (int64_t(ctx->sm_count) * 4));
+    if (smem_ok) chunk = std::max<int64_t>(chunk, bins * 2);
+    int64_t* cpc = arena<int64_t>(ctx, c.n_cells);
+    int64_t* item_off = arena<int64_t>(ctx, c.n_cells + 1);
+    VDFCG_LAUNCH(ctx, "cells_items",
+                 chunks_per_cell_kernel<<<std::max(1, std::min((c.n_cells + 255) / 256, 1024)), 256, 0,
+                                          ctx->stream>>>(c.offsets, c.n_cells, chunk, cpc));
+    launch_scan_i64(ctx, cpc, item_off, c.n_cells);
+    const int64_t est_items = (c.n + chunk - 1) / chunk + c.n_cells;
+    VelPtrs vp{{c.vel[0], c.vel[1], c.vel[2]}};
+    if (smem_ok) {
+      const size_t smem = static_cast<size_t>(bins) * 4;
+      auto k = cells_dense_kernel<D, true>;
+      VDFCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      int occ = 0;
+      VDFCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, block, smem));
+      const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(est_items, int64_t(ctx->sm_count) * std::max(occ, 1))));
+      VDFCG_LAUNCH(ctx, "cells_dense",
+                   k<<<grid, block, smem, ctx->stream>>>(vp, c.w, c.offsets, c.n_cells, item_off,
+                                                         chunk, g, bins, dense, densew, oor_cnt,
+                                                         oorw, err));
+    } else {
+      auto k = cells_dense_kernel<D, false>;
+      const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(est_items, int64_t(ctx->sm_count) * 2)));
+      VDFCG_LAUNCH(ctx, "cells_dense",
+                   k<<<grid, block, 0, ctx->stream>>>(vp, c.w, c.offsets, c.n_cells, item_off,
+                                                      chunk, g, bins, dense, densew, oor_cnt, oorw,
+                                                      err));
+    }
+    const int grid = std::max(1, std::min(c.n_cells, ctx->sm_count * 4));
+    if (weighted)
+      VDFCG_LAUNCH(ctx, "cells_compact",
+                   cells_compact_kernel<true><<<grid, 512, 0, ctx->stream>>>(
+                       c.n_cells, bins, dense, densew, oor_cnt, oorw, c.offsets, out.nnz, out.keys,
+                       out.counts, out.oor, out.in_range));
+    else
+      VDFCG_LAUNCH(ctx, "cells_compact",
+                   cells_compact_kernel<false><<<grid, 512, 0, ctx->stream>>>(
+                       c.n_cells, bins, dense, densew, oor_cnt, oorw, c.offsets, out.nnz, out.keys,
+                       out.counts, out.oor, out.in_range));
+  }
+  if (weighted) {
+    int* h = static_cast<int*>(ctx->pinned);
+    VDFCG_CUDA(cudaMemcpyAsync(h, err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    if (*h) throw InvalidArgument("particle weights must all be > 0");
+  }
+}
+
+void launch_bin_cells(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& out) {
+  if (c.n_cells == 0) return;
+  if (c.d == 2) bin_cells_d<2>(ctx, c, out);
+  else bin_cells_d<3>(ctx, c, out);
+}
+
+}  // namespace vdfcg

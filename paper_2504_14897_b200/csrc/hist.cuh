@@ -1,0 +1,47 @@
+// hist.cuh — histogram kernels (declarations of the host-side launchers).
+#pragma once
+
+#include "ctx.cuh"
+
+namespace vdfcg {
+
+// 2D marginal histograms over one pass (bin_particles: 1 plane; all_planes: 3 planes).
+// vel: N x d column-major device array. counts_out: nplanes * n^2 doubles, column-major
+// per plane. oor_out: nplanes doubles. Throws InvalidArgument on a non-positive weight.
+void launch_hist2d(vdfcg_ctx* ctx, const double* vel, int64_t n, int d, const double* w,
+                   int nplanes, const int* ax, const int* ay, int n_bins, const double* xlo,
+                   const double* xhi, const double* ylo, const double* yhi, double* counts_out,
+                   double* oor_out);
+
+// to_weighted_points on a column-major n x n count grid (device). Returns the count.
+int64_t launch_to_weighted_points(vdfcg_ctx* ctx, const double* counts, int n_bins, double xlo,
+                                  double xhi, double ylo, double yhi, bool drop_empty,
+                                  int64_t capacity, double* points, double* weights,
+                                  double* total_weight_dev);
+
+// Cell batch histogram + compaction (all pointers device).
+struct CellsDev {
+  int d;
+  int64_t n;
+  const double* vel[3];
+  const double* w;
+  int n_cells;
+  const int64_t* offsets;
+  int n_bins;
+  double lo[3], hi[3];
+};
+struct CellBinsDev {
+  int32_t* nnz;
+  uint32_t* keys;
+  double* counts;
+  double* oor;
+  double* in_range;
+};
+void launch_bin_cells(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& out);
+
+// Exclusive scan of n int64 values (device), total written to out[n].
+void launch_scan_i64(vdfcg_ctx* ctx, const int64_t* in, int64_t* out, int64_t n);
+// max over cells of (off[c+1]-off[c]) (device -> host, synchronizes).
+int64_t max_cell_size(vdfcg_ctx* ctx, const int64_t* offsets, int n_cells);
+
+}  // namespace vdfcg
