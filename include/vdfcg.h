@@ -273,12 +273,19 @@ int vdfcg_compress_cells(vdfcg_ctx* ctx, const vdfcg_cells* cells, const vdfcg_f
                          const vdfcg_model_meta* meta, uint8_t* records, int64_t capacity,
                          int64_t* record_offsets);
 
-/* Synthetic cell data for tests/bench (counter-based, deterministic per (seed, cell)):
- * each cell draws from a 2-component mixture whose drift/temperature vary with the
- * cell index. Device pointers only. */
+/* Synthetic cell data for tests/bench (counter-based, deterministic per (seed, species,
+ * global particle index)): each cell draws from a 2-component mixture whose drift and
+ * temperature vary with the global cell index. cell_offsets are GLOBAL particle offsets
+ * of cells [cell_base, cell_base + n_cells); particle p is written at p - cell_offsets[0].
+ * Device pointers only. */
 int vdfcg_synth_cells(vdfcg_ctx* ctx, int32_t dimension, int32_t n_cells,
-                      const int64_t* cell_offsets, uint64_t seed, int32_t species,
-                      double* velocity_u, double* velocity_v, double* velocity_w);
+                      const int64_t* cell_offsets, int64_t cell_base, uint64_t seed,
+                      int32_t species, double* velocity_u, double* velocity_v,
+                      double* velocity_w);
+
+/* Roofline denominators: FP64 and FP32 FMA throughput of this device, measured with a
+ * dependent-chain-free FMA loop on every SM (TFLOP/s, FMA = 2 flops). */
+int vdfcg_probe_peaks(vdfcg_ctx* ctx, double* fp64_tflops, double* fp32_tflops);
 
 #ifdef __cplusplus
 }

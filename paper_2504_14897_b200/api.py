@@ -56,7 +56,8 @@ def _bind(lib) -> None:
         "vdfcg_fit_cells": (C.c_int, [vp, vp, vp, vp, vp]),
         "vdfcg_pack_cells": (C.c_int, [vp, i32, i32, vp, vp, vp, i64, vp]),
         "vdfcg_compress_cells": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, i64, vp]),
-        "vdfcg_synth_cells": (C.c_int, [vp, i32, i32, vp, u64, i32, vp, vp, vp]),
+        "vdfcg_synth_cells": (C.c_int, [vp, i32, i32, vp, i64, u64, i32, vp, vp, vp]),
+        "vdfcg_probe_peaks": (C.c_int, [vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -180,6 +181,13 @@ def default_axis_range(particles: ParticleSet, axis: int) -> AxisRange:
     """histogram.cpp:27-30: +/- 5 nominal thermal speeds."""
     vth = float(np.sqrt(particles.nominal_temperature[axis]))
     return AxisRange(-5.0 * vth, 5.0 * vth)
+
+
+def probe_peaks() -> tuple[float, float]:
+    """Measured (FP64, FP32) FMA TFLOP/s of the current device (roofline denominators)."""
+    f64, f32 = C.c_double(0.0), C.c_double(0.0)
+    _marshal.check(lib().vdfcg_probe_peaks(context().handle, C.byref(f64), C.byref(f32)), last_error)
+    return f64.value, f32.value
 
 
 def validate_fit_config(config: FitConfig, d: int) -> None:

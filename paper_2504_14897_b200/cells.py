@@ -239,9 +239,12 @@ def compress_cells(batch: CellBatch, config: FitConfig, meta: Optional[ModelMeta
     return bins, results, rec, offs
 
 
-def synth_cells(d: int, cell_offsets, seed: int, species: int, u, v, w=None) -> None:
-    """Deterministic synthetic plasma cells into device tensors (tests/bench data)."""
+def synth_cells(d: int, cell_offsets, seed: int, species: int, u, v, w=None,
+                cell_base: int = 0) -> None:
+    """Deterministic synthetic plasma cells into device tensors (tests/bench data).
+    cell_offsets: GLOBAL particle offsets of cells [cell_base, cell_base + n)."""
     api = _api()
     _check(api.lib().vdfcg_synth_cells(api.context().handle, d, int(cell_offsets.shape[0]) - 1,
-                                       _ptr(cell_offsets), seed & 0xFFFFFFFFFFFFFFFF, species,
-                                       _ptr(u), _ptr(v), _ptr(w)))
+                                       _ptr(cell_offsets), int(cell_base),
+                                       seed & 0xFFFFFFFFFFFFFFFF, species, _ptr(u), _ptr(v),
+                                       _ptr(w)))

@@ -16,8 +16,10 @@
 #include "pack.cuh"
 
 namespace vdfcg {
-void launch_synth(vdfcg_ctx* ctx, int d, int n_cells, const int64_t* offsets, uint64_t seed,
-                  int species, double* u, double* v, double* w);
+void launch_synth(vdfcg_ctx* ctx, int d, int n_cells, const int64_t* offsets, int64_t cell_base,
+                  uint64_t seed, int species, double* u, double* v, double* w);
+double probe_fp64(vdfcg_ctx* ctx);
+double probe_fp32(vdfcg_ctx* ctx);
 
 namespace {
 
@@ -865,14 +867,23 @@ int vdfcg_compress_cells(vdfcg_ctx* ctx, const vdfcg_cells* cells, const vdfcg_f
 }
 
 int vdfcg_synth_cells(vdfcg_ctx* ctx, int32_t d, int32_t n_cells, const int64_t* cell_offsets,
-                      uint64_t seed, int32_t species, double* u, double* v, double* w) {
+                      int64_t cell_base, uint64_t seed, int32_t species, double* u, double* v,
+                      double* w) {
   return guard_impl([&] {
     begin(ctx);
     if (d != 2 && d != 3) throw InvalidArgument("dimension must be 2 or 3");
     if (!is_device_pointer(cell_offsets) || !is_device_pointer(u) || !is_device_pointer(v) ||
         (d == 3 && !is_device_pointer(w)))
       throw InvalidArgument("vdfcg_synth_cells takes device pointers");
-    if (n_cells > 0) launch_synth(ctx, d, n_cells, cell_offsets, seed, species, u, v, w);
+    if (n_cells > 0) launch_synth(ctx, d, n_cells, cell_offsets, cell_base, seed, species, u, v, w);
+  });
+}
+
+int vdfcg_probe_peaks(vdfcg_ctx* ctx, double* fp64, double* fp32) {
+  return guard_impl([&] {
+    begin(ctx);
+    if (fp64) *fp64 = probe_fp64(ctx);
+    if (fp32) *fp32 = probe_fp32(ctx);
   });
 }
 
