@@ -44,15 +44,18 @@ struct EmState {
   double Lo[K][3];  // L(1,0), L(2,0), L(2,1)
   double rd[K][3];  // 1 / L(a,a)
   double cst[K];    // -0.5 (d log 2pi + log det) + log alpha ; -inf when dead
+  double A[K][6];   // L^-1 packed (affine form used by the point pass)
+  double bv[K][3];  // L^-1 mu
   double mu_new[K][D];
   double sig1[K][9];
   double st[K][NS];
   double st2[K][NS];
+  double exp2tab[64];
   double ll;
   double prev_ll;
   Frame fr;
-  int m, status, err_id, converged, dead_mask, degen_mask, exact_mask, n_events, it_used, cell,
-      stop;
+  int m, status, err_id, converged, dead_mask, degen_mask, exact_mask, cert_mask, n_events,
+      it_used, cell, stop;
   int minidx[3], maxidx[3];
 };
 
@@ -68,12 +71,13 @@ struct KeySrc {
   const uint32_t* keys;
   const double* counts;
   int nb;
+  uint32_t magic;      // ceil(2^32 / nb): exact quotient for keys < 2^32 / nb (nb <= 255)
   const double* ztab;  // shared [D][nb]
   VDFCG_DEV void load(int p, double (&z)[D], double& w) const {
     uint32_t k = __ldg(keys + p);
 #pragma unroll
     for (int a = D - 1; a >= 0; --a) {
-      const uint32_t q = k / static_cast<uint32_t>(nb);
+      const uint32_t q = magic ? __umulhi(k, magic) : k / static_cast<uint32_t>(nb);
       const uint32_t idx = k - q * static_cast<uint32_t>(nb);
       z[a] = ztab[a * nb + idx];
       k = q;
@@ -120,7 +124,7 @@ VDFCG_DEV void em_pass(const Src& src, int n, EmState<D, K>& S, double* red) {
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       if (i < m) {
-        lp[i] = comp_logp<D>(z, S.mu[i], S.Lo[i], S.rd[i], S.cst[i]);
+        lp[i] = comp_logp_affine<D>(z, S.A[i], S.bv[i], S.cst[i]);
         mx = fmax(mx, lp[i]);
       }
     }
@@ -128,12 +132,12 @@ VDFCG_DEV void em_pass(const Src& src, int n, EmState<D, K>& S, double* red) {
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       if (i < m) {
-        lp[i] = exp(lp[i] - mx);
+        lp[i] = exp_nonpos(lp[i] - mx, S.exp2tab);
         s += lp[i];
       }
     }
     if (!EXACT) ll.add(w * (mx + log(s)));
-    const double ws = w / s;
+    const double ws = w * rcp_newton(s);
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       if (i < m) {
@@ -214,7 +218,10 @@ VDFCG_DEV void run_fit(const Src& src, int n, EmState<D, K>& S, double* red, con
     // ---- E-step preparation: one lane per component (wgmm.cpp:197-229)
     if (warp == 0) {
       bool dead = false;
-      if (lane < S.m) dead = !prep_component<D>(S.cov[lane], S.alpha[lane], S.Lo[lane], S.rd[lane], &S.cst[lane]);
+      if (lane < S.m) {
+        dead = !prep_component<D>(S.cov[lane], S.alpha[lane], S.Lo[lane], S.rd[lane], &S.cst[lane]);
+        affine_from_chol<D>(S.mu[lane], S.Lo[lane], S.rd[lane], S.A[lane], S.bv[lane]);
+      }
       const unsigned dm = __ballot_sync(0xffffffffu, dead);
       if (lane == 0) {
         S.dead_mask = static_cast<int>(dm);
@@ -232,18 +239,19 @@ VDFCG_DEV void run_fit(const Src& src, int n, EmState<D, K>& S, double* red, con
 
     // ---- M-step part 1 (wgmm.cpp:269-298)
     if (warp == 0) {
-      bool bad = false, need = false;
+      bool bad = false, need = false, cert = false;
       if (lane < S.m) {
         const int i = lane;
         const double mass = S.st[i][0];
         bad = !isfinite(mass) || mass < 0.0;
         const bool starved = !(mass > S.fr.total * kMassFloorRel);
         if (!bad && !starved) {
+          const double inv = 1.0 / mass;
           double db[D];
           double dd = 0.0;
 #pragma unroll
           for (int a = 0; a < D; ++a) {
-            db[a] = S.st[i][1 + a] / mass;
+            db[a] = S.st[i][1 + a] * inv;
             S.mu_new[i][a] = S.mu[i][a] + db[a];
             dd += db[a] * db[a];
           }
@@ -254,21 +262,24 @@ VDFCG_DEV void run_fit(const Src& src, int n, EmState<D, K>& S, double* red, con
           for (int a = 0; a < D; ++a)
 #pragma unroll
             for (int b = a; b < D; ++b)
-              s1(a, b) = S.st[i][1 + D + uidx<D>(a, b)] / mass - db[a] * db[b];
+              s1(a, b) = S.st[i][1 + D + uidx<D>(a, b)] * inv - db[a] * db[b];
           symmetrize_from_upper<D>(s1);
 #pragma unroll
           for (int e = 0; e < 9; ++e) S.sig1[i][e] = s1.a[e];
           // The shifted form loses ~eps*|d|^2 absolute; recompute Eq. 9 around the new
-          // mean whenever that could reach 1e-12 of the smallest eigenvalue or the
-          // component is near collapse, so the collapse test sees reference numerics.
-          const double lmin = min_eigenvalue<D>(s1);
-          need = !(lmin > 0.0) || dd > 1e3 * lmin;
+          // mean whenever that could reach 1e-12 of the smallest eigenvalue (or the LLT
+          // fails), so the collapse test sees reference-grade numerics. lmin >= lb.
+          const double lb = lmin_lower_bound<D>(s1);
+          need = !(lb > 0.0) || dd > 1e3 * lb;
+          cert = lb > 1e-14 * trace3<D>(s1);
         }
       }
       const unsigned bm = __ballot_sync(0xffffffffu, bad);
       const unsigned nm = __ballot_sync(0xffffffffu, need);
+      const unsigned cm = __ballot_sync(0xffffffffu, cert);
       if (lane == 0) {
         S.exact_mask = static_cast<int>(nm);
+        S.cert_mask = static_cast<int>(cm);
         if (bm) {
           S.status = VDFCG_RUNTIME_ERROR;
           S.err_id = kMsgInvalidMass;
@@ -289,21 +300,28 @@ VDFCG_DEV void run_fit(const Src& src, int n, EmState<D, K>& S, double* red, con
         const bool starved = !(mass > S.fr.total * kMassFloorRel);
         if (!starved) {
           Sym3 sg;
+          bool certified;
           if ((S.exact_mask >> i) & 1) {
 #pragma unroll
             for (int e = 0; e < 9; ++e) sg.a[e] = 0.0;
+            const double inv = 1.0 / mass;
 #pragma unroll
             for (int a = 0; a < D; ++a)
 #pragma unroll
-              for (int b = a; b < D; ++b) sg(a, b) = S.st2[i][1 + D + uidx<D>(a, b)] / mass;
+              for (int b = a; b < D; ++b) sg(a, b) = S.st2[i][1 + D + uidx<D>(a, b)] * inv;
             symmetrize_from_upper<D>(sg);
+            certified = lmin_lower_bound<D>(sg) > 1e-14 * trace3<D>(sg);
           } else {
             load_cov<D>(S.sig1[i], sg);
+            certified = (S.cert_mask >> i) & 1;
           }
 #pragma unroll
           for (int a = 0; a < D; ++a) S.mu[i][a] = S.mu_new[i][a];
           Sym3 acc;
-          if (accept_covariance<D>(sg, acc)) {
+          if (certified) {
+#pragma unroll
+            for (int e = 0; e < 9; ++e) S.cov[i][e] = sg.a[e];
+          } else if (accept_covariance<D>(sg, acc)) {
 #pragma unroll
             for (int e = 0; e < 9; ++e) S.cov[i][e] = acc.a[e];
           } else {
@@ -416,6 +434,8 @@ VDFCG_DEV int key_prologue(const KeyCells& kc, int c, const EmConfig& cfg, EmSta
   src.keys = kc.keys + base;
   src.counts = kc.counts + base;
   src.nb = nb;
+  // n^d * (magic*n - 2^32) < 2^32 keeps umulhi exact for every key (holds for n <= 255)
+  src.magic = (D == 3 ? nb <= 255 : nb <= 1625) ? static_cast<uint32_t>((0x100000000ULL + nb - 1) / nb) : 0u;
   src.ztab = ztab;
   if (threadIdx.x == 0) {
     S.status = 0;
@@ -553,7 +573,7 @@ VDFCG_DEV int key_prologue(const KeyCells& kc, int c, const EmConfig& cfg, EmSta
 }
 
 template <int D, int K, bool KEYS>
-__global__ void __launch_bounds__(256) em_kernel(KeyCells kc, CoordArgs ca, EmConfig cfg,
+__global__ void __launch_bounds__(256, (K <= 4 ? 2 : 1)) em_kernel(KeyCells kc, CoordArgs ca, EmConfig cfg,
                                                  EmOut out, int* counter, int red_stride) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   EmState<D, K>& S = *reinterpret_cast<EmState<D, K>*>(smem_raw);
@@ -561,6 +581,7 @@ __global__ void __launch_bounds__(256) em_kernel(KeyCells kc, CoordArgs ca, EmCo
   double* red = reinterpret_cast<double*>(smem_raw + st_bytes);
   double* ztab = red + (blockDim.x >> 5) * red_stride;
   const int n_cells = KEYS ? kc.n_cells : 1;
+  for (int j = threadIdx.x; j < 64; j += blockDim.x) S.exp2tab[j] = kExp2Tab[j];
   for (;;) {
     if (threadIdx.x == 0) S.cell = atomicAdd(counter, 1);
     __syncthreads();
@@ -868,10 +889,14 @@ static void launch_em_k(vdfcg_ctx* ctx, int K, const KeyCells& kc, const CoordAr
 
 // Warps per fit: enough lanes that each holds ~16 points per pass, and enough CTAs in
 // flight to fill every SM; deterministic in the input shape only.
+// Warps per fit. Small fits (the cfg4 regime, <= ~4K non-empty bins) get one warp each:
+// the per-iteration serial part (M-step, protocol) then stalls only its own warp while
+// the other resident fits keep the FP64 pipe busy. Larger fits get up to 8 warps, and
+// few fits are widened so the grid still fills every SM. Depends on the input shape only.
 static int choose_warps(double pts_per_fit, int n_fits, int sm_count) {
   int G = 1;
-  while (G < 8 && pts_per_fit / (32.0 * G) > 16.0) G *= 2;
-  while (G < 8 && double(n_fits) * G < sm_count * 8.0 && pts_per_fit / (32.0 * G) > 2.0) G *= 2;
+  while (G < 8 && pts_per_fit / (32.0 * G) > 128.0) G *= 2;
+  while (G < 8 && double(n_fits) * G < sm_count * 12.0 && pts_per_fit / (32.0 * G) > 8.0) G *= 2;
   return G;
 }
 

@@ -39,18 +39,76 @@ VDFCG_DEV bool prep_component(double* cov9, double alpha, double* Lo, double* rd
     }
     return false;
   }
-  double logdet_half = 0.0;
+  double prodL = 1.0;
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     rd[a] = 1.0 / L(a, a);
-    logdet_half += log(L(a, a));
+    prodL *= L(a, a);
   }
   Lo[0] = D >= 2 ? L(1, 0) : 0.0;
   Lo[1] = D >= 3 ? L(2, 0) : 0.0;
   Lo[2] = D >= 3 ? L(2, 1) : 0.0;
-  const double la = alpha > 0.0 ? log(alpha) : -dinf();
-  *cst = -0.5 * (D * kLog2Pi + 2.0 * logdet_half) + la;
+  // -0.5 (d log 2pi + 2 sum log L_aa) + log alpha, with one log
+  *cst = alpha > 0.0 ? -0.5 * D * kLog2Pi + log(alpha / prodL) : -dinf();
   return true;
+}
+
+// 2^(j/64), j = 0..63, correctly rounded (50-digit decimal evaluation).
+__device__ __constant__ double kExp2Tab[64] = {
+    1.0, 1.0108892860517005, 1.0218971486541166, 1.0330248790212284,
+    1.0442737824274138, 1.0556451783605572, 1.0671404006768237, 1.0787607977571199,
+    1.0905077326652577, 1.102382583307841, 1.1143867425958924, 1.1265216186082418,
+    1.1387886347566916, 1.1511892299529827, 1.1637248587775775, 1.1763969916502812,
+    1.189207115002721, 1.202156731452703, 1.215247359980469, 1.22848053610687,
+    1.241857812073484, 1.255380757024691, 1.2690509571917332, 1.2828700160787783,
+    1.2968395546510096, 1.3109612115247644, 1.3252366431597413, 1.339667524053303,
+    1.3542555469368927, 1.3690024229745905, 1.383909881963832, 1.3989796725383112,
+    1.4142135623730951, 1.42961333839197, 1.4451808069770467, 1.460917794180647,
+    1.4768261459394993, 1.4929077282912648, 1.5091644275934228, 1.5255981507445384,
+    1.5422108254079407, 1.559004400237837, 1.5759808451078865, 1.593142151342267,
+    1.6104903319492543, 1.6280274218573478, 1.645755478153965, 1.6636765803267364,
+    1.681792830507429, 1.7001063537185235, 1.718619298122478, 1.7373338352737062,
+    1.7562521603732995, 1.7753764925265212, 1.7947090750031072, 1.8142521755003989,
+    1.8340080864093424, 1.8539791250833855, 1.8741676341103, 1.8945759815869656,
+    1.9152065613971474, 1.9360617934922943, 1.9571441241754002, 1.978456026387951};
+
+// Polynomial / reduction constants live in the constant bank so FP64 instructions take
+// them as c[][] operands instead of rematerialising 64-bit literals every iteration.
+__device__ __constant__ double kExpC[8] = {
+    92.33248261689366,        // 64 / ln 2
+    6755399441055744.0,       // 1.5 * 2^52 (round-to-nearest-integer shifter)
+    0.010830424696249145,     // ln2/64, high part
+    3.6235106466348431e-19,   // ln2/64, low part
+    1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 0.5};
+
+// exp(x) for x <= 0 (x = log p - max log p in the E-step), accurate to ~1 ulp:
+// x = (64 q + j) ln2/64 + r with |r| <= ln2/128 (FMA Cody-Waite), 2^(j/64) from a
+// 64-entry shared table, degree-5 Taylor for e^r (truncation 3e-17). x is clamped at
+// -708 (e^-708 ~ 3e-308: such responsibilities are below every tolerance; the reference
+// would produce the same value or a subnormal).
+VDFCG_DEV double exp_nonpos(double x, const double* tab) {
+  x = fmax(x, -708.0);
+  const double tm = fma(x, kExpC[0], kExpC[1]);
+  const int k = __double2loint(tm);
+  const double kd = tm - kExpC[1];
+  double r = fma(-kd, kExpC[2], x);
+  r = fma(-kd, kExpC[3], r);
+  double p = fma(r, kExpC[4], kExpC[5]);
+  p = fma(p, r, kExpC[6]);
+  p = fma(p, r, kExpC[7]);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const double scale = __hiloint2double(((k >> 6) + 1023) << 20, 0);
+  return (tab[k & 63] * p) * scale;
+}
+
+// 1/s for s >= 1 (the per-point mixture normaliser): MUFU estimate + 2 Newton steps.
+VDFCG_DEV double rcp_newton(double s) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(s));
+  r = fma(r, fma(-s, r, 1.0), r);
+  r = fma(r, fma(-s, r, 1.0), r);
+  return r;
 }
 
 // log N(z | mu, L) + log alpha for one component (prepared by prep_component).
@@ -65,6 +123,40 @@ VDFCG_DEV double comp_logp(const double* z, const double* mu, const double* Lo, 
   if (D >= 2) q += y1 * y1;
   if (D >= 3) q += y2 * y2;
   return cst - 0.5 * q;
+}
+
+// The same density through y = A z - b with A = L^-1 (lower triangular), b = A mu:
+// 6 FMAs instead of 3 subtractions + the substitution (used by the fused point pass).
+// A is packed {a00, a10, a11, a20, a21, a22}.
+template <int D>
+VDFCG_DEV void affine_from_chol(const double* mu, const double* Lo, const double* rd, double* A,
+                                double* b) {
+  // rows of L^-1 by forward substitution on the unit vectors
+  const double a00 = rd[0];
+  const double a10 = D >= 2 ? -Lo[0] * a00 * rd[1] : 0.0;
+  const double a11 = D >= 2 ? rd[1] : 0.0;
+  const double a20 = D >= 3 ? -(Lo[1] * a00 + Lo[2] * a10) * rd[2] : 0.0;
+  const double a21 = D >= 3 ? -Lo[2] * a11 * rd[2] : 0.0;
+  const double a22 = D >= 3 ? rd[2] : 0.0;
+  A[0] = a00; A[1] = a10; A[2] = a11; A[3] = a20; A[4] = a21; A[5] = a22;
+  b[0] = a00 * mu[0];
+  b[1] = D >= 2 ? a10 * mu[0] + a11 * mu[1] : 0.0;
+  b[2] = D >= 3 ? a20 * mu[0] + a21 * mu[1] + a22 * mu[2] : 0.0;
+}
+
+template <int D>
+VDFCG_DEV double comp_logp_affine(const double* z, const double* A, const double* b, double cst) {
+  const double y0 = fma(A[0], z[0], -b[0]);
+  double q = y0 * y0;
+  if (D >= 2) {
+    const double y1 = fma(A[2], z[1], fma(A[1], z[0], -b[1]));
+    q = fma(y1, y1, q);
+  }
+  if (D >= 3) {
+    const double y2 = fma(A[5], z[2], fma(A[4], z[1], fma(A[3], z[0], -b[2])));
+    q = fma(y2, y2, q);
+  }
+  return fma(-0.5, q, cst);
 }
 
 // Model arrays: alpha[K], mu[K*D], cov[K*9] (3x3 slots).

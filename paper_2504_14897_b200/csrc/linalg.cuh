@@ -161,6 +161,35 @@ VDFCG_DEV bool accept_covariance(const Sym3& sigma, Sym3& out) {
   return true;
 }
 
+// Cheap certificate for the collapse test (wgmm.cpp:305-306): if the LLT of sigma
+// succeeds, det = prod(L_aa)^2 and lambda_min >= det / prod of the other eigenvalues
+// >= det / (tr/2)^2 (d=3) or det / tr (d=2). When that lower bound already exceeds
+// 1e-14 * tr (>= 1e-14 * lambda_max) the component certainly did not collapse and
+// repair_covariance would return sigma unchanged (doublings = -1), so the reference
+// sequence "eigen test, then repair" reduces to "accept sigma". Returns the bound
+// (or -1 when the LLT fails); the caller falls back to accept_covariance otherwise.
+template <int D>
+VDFCG_DEV double lmin_lower_bound(const Sym3& s) {
+  Sym3 L;
+  if (!cholesky<D>(s, L)) return -1.0;
+  double p = 1.0, tr = 0.0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    p *= L(a, a);
+    tr += s(a, a);
+  }
+  const double det = p * p;
+  return D == 1 ? det : (D == 2 ? det / tr : det / (0.25 * tr * tr));
+}
+
+template <int D>
+VDFCG_DEV double trace3(const Sym3& s) {
+  double tr = 0.0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) tr += s(a, a);
+  return tr;
+}
+
 // Smallest eigenvalue estimate used to decide whether the one-pass shifted covariance
 // needs the exact second pass (see em.cu).
 template <int D>
