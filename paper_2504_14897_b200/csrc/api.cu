@@ -159,6 +159,7 @@ CellsDev stage_cells(vdfcg_ctx* ctx, const vdfcg_cells* cells) {
   double nbd = 1.0;
   for (int a = 0; a < d; ++a) nbd *= cells->n_bins;
   if (nbd > 2147483647.0) throw InvalidArgument("n_bins^d must fit a 31-bit bin key");
+  if (d == 3 && cells->n_bins > 1024) throw InvalidArgument("3V cells support n_bins <= 1024");
   for (int a = 0; a < d; ++a)
     if (!range_ok(cells->lo[a], cells->hi[a]))
       throw InvalidArgument("axis range must satisfy min < max");
@@ -743,6 +744,7 @@ static void fit_cells_dev(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& 
   kc.keys = b.keys;
   kc.counts = b.counts;
   kc.in_range = b.in_range;
+  kc.packed = arena<uint32_t>(ctx, size_t(std::max<int64_t>(c.n, 1)));
   kc.n_bins = c.n_bins;
   for (int a = 0; a < 3; ++a) {
     kc.lo[a] = c.lo[a];

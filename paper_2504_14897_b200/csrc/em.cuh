@@ -70,8 +70,16 @@ struct KeyCells {
   const uint32_t* keys;
   const double* counts;
   const double* in_range;
+  uint32_t* packed;        // scratch [n_particles]: decoded bin indices (device)
   int n_bins;
   double lo[3], hi[3];
+};
+
+struct CoordArgs {
+  const double* z;  // SoA normalized points [D][n]
+  int64_t n;
+  const double* w;
+  const Frame* frame;
 };
 
 // uniforms[0..n) = mt19937_64(seed) top-53-bit doubles (rng.hpp:22), on the device.

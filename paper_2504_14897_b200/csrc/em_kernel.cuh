@@ -1,0 +1,650 @@
+// em_kernel.cuh — the fused batched weighted-EM kernel (K5) as templates over the
+// velocity dimension D and the component capacity K. Instantiated per D in em_d2.cu /
+// em_d3.cu so the exact-K variants compile in parallel. See em.cu for the overview.
+#pragma once
+
+#include <cub/block/block_reduce.cuh>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "em.cuh"
+#include "em_dev.cuh"
+#include "linalg.cuh"
+
+namespace vdfcg {
+
+template <int D>
+struct NStat {
+  static constexpr int value = 1 + D + D * (D + 1) / 2;
+};
+
+template <int D, int K>
+struct EmState {
+  static constexpr int NS = NStat<D>::value;
+  double alpha[K];
+  double mu[K][D];
+  double cov[K][9];
+  double Lo[K][3];  // L(1,0), L(2,0), L(2,1)
+  double rd[K][3];  // 1 / L(a,a)
+  double cst[K];    // -0.5 (d log 2pi + log det) + log alpha ; -inf when dead
+  double A[K][6];   // L^-1 packed (affine form used by the point pass)
+  double bv[K][3];  // L^-1 mu
+  double mu_new[K][D];
+  double sig1[K][9];
+  double st[K][NS];
+  double st2[K][NS];
+  double exp2tab[64];
+  double ll;
+  double prev_ll;
+  Frame fr;
+  int m, status, err_id, converged, dead_mask, degen_mask, exact_mask, cert_mask, n_events,
+      it_used, cell, stop;
+  int minidx[3], maxidx[3];
+};
+
+
+template <int D>
+struct KeySrc {
+  // bin indices decoded once per fit (prologue) into packed fields: axis a at bit
+  // a * SHIFT (10 bits for d=3, 16 for d=2), so the point pass only shifts and masks.
+  static constexpr int SHIFT = D == 3 ? 10 : 16;
+  static constexpr uint32_t MASK = (1u << SHIFT) - 1u;
+  const uint32_t* keys;
+  uint32_t* packed;
+  const double* counts;
+  int nb;
+  const double* ztab;  // shared [D][nb]
+  VDFCG_DEV void load(int p, double (&z)[D], double& w) const {
+    const uint32_t k = packed[p];
+#pragma unroll
+    for (int a = 0; a < D; ++a) z[a] = ztab[a * nb + ((k >> (SHIFT * a)) & MASK)];
+    w = __ldg(counts + p);
+  }
+};
+
+template <int D>
+struct CoordSrc {
+  const double* z;
+  int64_t n;
+  const double* w;
+  VDFCG_DEV void load(int p, double (&zz)[D], double& ww) const {
+#pragma unroll
+    for (int a = 0; a < D; ++a) zz[a] = __ldg(z + a * n + p);
+    ww = __ldg(w + p);
+  }
+};
+
+template <int D>
+VDFCG_DEV constexpr int uidx(int a, int b) {  // packed upper index, a <= b
+  return D == 2 ? (a == 0 ? b : 2) : (a == 0 ? b : (a == 1 ? 2 + b : 5));
+}
+
+// ---------------------------------------------------------------- the point pass
+// EXACT=false: pass 1, statistics centred on mu_old (+ loglik). EXACT=true: the
+// covariance sums centred on mu_new for the components flagged in exact_mask.
+template <int D, int K, bool EXACT, class Src>
+VDFCG_DEV void em_pass(const Src& src, int n, EmState<D, K>& S, double* red) {
+  constexpr int NS = NStat<D>::value;
+  const int m = S.m;
+  double acc[K][NS];
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < NS; ++j) acc[i][j] = 0.0;
+  Kahan ll;
+  for (int p = threadIdx.x; p < n; p += blockDim.x) {
+    double z[D], w;
+    src.load(p, z, w);
+    // Every slot i < K is evaluated: slots >= m carry cst = -inf, A = b = mu = 0, so they
+    // add exactly nothing to s and their accumulators are never read (no per-slot branch).
+    double lp[K];
+    double mx = -dinf();
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      lp[i] = comp_logp_affine<D>(z, S.A[i], S.bv[i], S.cst[i]);
+      mx = fmax(mx, lp[i]);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      lp[i] = exp_nonpos(lp[i] - mx, S.exp2tab);
+      s += lp[i];
+    }
+    if (!EXACT) ll.add(w * (mx + log(s)));
+    const double ws = w * rcp_newton(s);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      {
+        if (EXACT && !((S.exact_mask >> i) & 1)) continue;
+        const double g = lp[i] * ws;
+        double dl[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) dl[a] = z[a] - (EXACT ? S.mu_new[i][a] : S.mu[i][a]);
+        acc[i][0] += g;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          const double gd = g * dl[a];
+          acc[i][1 + a] += gd;
+#pragma unroll
+          for (int b = a; b < D; ++b) acc[i][1 + D + uidx<D>(a, b)] += gd * dl[b];
+        }
+      }
+    }
+  }
+  // fixed-order reduction: lanes (xor tree) -> warps (ascending)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, G = blockDim.x >> 5;
+  constexpr int W = K * NS + 1;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    if (i < m) {
+#pragma unroll
+      for (int j = 0; j < NS; ++j) {
+        const double v = warp_sum(acc[i][j]);
+        if (lane == 0) red[warp * W + i * NS + j] = v;
+      }
+    }
+  }
+  if (!EXACT) {
+    const double v = warp_sum(ll.value());
+    if (lane == 0) red[warp * W + K * NS] = v;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < W; t += blockDim.x) {
+    if (t < K * NS) {
+      const int i = t / NS;
+      if (i >= m) continue;
+      double sum = 0.0;
+      for (int g = 0; g < G; ++g) sum += red[g * W + t];
+      if (EXACT) S.st2[i][t % NS] = sum; else S.st[i][t % NS] = sum;
+    } else if (!EXACT) {
+      double sum = 0.0;
+      for (int g = 0; g < G; ++g) sum += red[g * W + t];
+      S.ll = sum;
+    }
+  }
+  __syncthreads();
+}
+
+template <int D>
+VDFCG_DEV void load_cov(const double* c9, Sym3& s) {
+#pragma unroll
+  for (int e = 0; e < 9; ++e) s.a[e] = c9[e];
+}
+
+// ---------------------------------------------------------------- the fit
+template <int D, int K, class Src>
+VDFCG_DEV void run_fit(const Src& src, int n, EmState<D, K>& S, double* red, const EmConfig& cfg,
+                       const EmOut& out, int c) {
+  constexpr int NS = NStat<D>::value;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // ---- init (wgmm.cpp:136-191)
+  if (threadIdx.x == 0) {
+    S.n_events = 0;
+    S.converged = 0;
+    S.stop = 0;
+    S.it_used = 0;
+    S.prev_ll = dnan();
+    if (!S.status) S.m = init_model_dev<D>(S.fr, cfg, S.alpha, &S.mu[0][0], &S.cov[0][0]);
+  }
+  __syncthreads();
+
+  for (int it = 1; it <= cfg.max_it && !S.status; ++it) {
+    // ---- E-step preparation: one lane per component (wgmm.cpp:197-229)
+    if (warp == 0) {
+      bool dead = false;
+      if (lane < S.m) {
+        dead = !prep_component<D>(S.cov[lane], S.alpha[lane], S.Lo[lane], S.rd[lane], &S.cst[lane]);
+        affine_from_chol<D>(S.mu[lane], S.Lo[lane], S.rd[lane], S.A[lane], S.bv[lane]);
+      } else if (lane < K) {  // inactive slot: contributes exactly zero
+        S.cst[lane] = -dinf();
+#pragma unroll
+        for (int e = 0; e < 6; ++e) S.A[lane][e] = 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) S.bv[lane][a] = 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) S.mu[lane][a] = 0.0;
+      }
+      const unsigned dm = __ballot_sync(0xffffffffu, dead);
+      if (lane == 0) {
+        S.dead_mask = static_cast<int>(dm);
+        if (S.m > 0 && __popc(dm) == S.m) {
+          S.status = VDFCG_RUNTIME_ERROR;
+          S.err_id = kMsgAllDegenerate;
+        }
+      }
+    }
+    __syncthreads();
+    if (S.status) break;
+
+    // ---- E-step + sufficient statistics (one pass over the points)
+    em_pass<D, K, false>(src, n, S, red);
+
+    // ---- M-step part 1 (wgmm.cpp:269-298)
+    if (warp == 0) {
+      bool bad = false, need = false, cert = false;
+      if (lane < S.m) {
+        const int i = lane;
+        const double mass = S.st[i][0];
+        bad = !isfinite(mass) || mass < 0.0;
+        const bool starved = !(mass > S.fr.total * kMassFloorRel);
+        if (!bad && !starved) {
+          const double inv = 1.0 / mass;
+          double db[D];
+          double dd = 0.0;
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            db[a] = S.st[i][1 + a] * inv;
+            S.mu_new[i][a] = S.mu[i][a] + db[a];
+            dd += db[a] * db[a];
+          }
+          Sym3 s1;
+#pragma unroll
+          for (int e = 0; e < 9; ++e) s1.a[e] = 0.0;
+#pragma unroll
+          for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int b = a; b < D; ++b)
+              s1(a, b) = S.st[i][1 + D + uidx<D>(a, b)] * inv - db[a] * db[b];
+          symmetrize_from_upper<D>(s1);
+#pragma unroll
+          for (int e = 0; e < 9; ++e) S.sig1[i][e] = s1.a[e];
+          // The shifted form loses ~eps*|d|^2 absolute; recompute Eq. 9 around the new
+          // mean whenever that could reach 1e-12 of the smallest eigenvalue (or the LLT
+          // fails), so the collapse test sees reference-grade numerics. lmin >= lb.
+          const double lb = lmin_lower_bound<D>(s1);
+          need = !(lb > 0.0) || dd > 1e3 * lb;
+          cert = lb > 1e-14 * trace3<D>(s1);
+        }
+      }
+      const unsigned bm = __ballot_sync(0xffffffffu, bad);
+      const unsigned nm = __ballot_sync(0xffffffffu, need);
+      const unsigned cm = __ballot_sync(0xffffffffu, cert);
+      if (lane == 0) {
+        S.exact_mask = static_cast<int>(nm);
+        S.cert_mask = static_cast<int>(cm);
+        if (bm) {
+          S.status = VDFCG_RUNTIME_ERROR;
+          S.err_id = kMsgInvalidMass;
+        }
+      }
+    }
+    __syncthreads();
+    if (S.status) break;
+    if (S.exact_mask) em_pass<D, K, true>(src, n, S, red);
+
+    // ---- M-step part 2: covariances, collapse test, repair (wgmm.cpp:299-316)
+    if (warp == 0) {
+      bool degen = false;
+      if (lane < S.m) {
+        const int i = lane;
+        const double mass = S.st[i][0];
+        S.alpha[i] = mass / S.fr.total;
+        const bool starved = !(mass > S.fr.total * kMassFloorRel);
+        if (!starved) {
+          Sym3 sg;
+          bool certified;
+          if ((S.exact_mask >> i) & 1) {
+#pragma unroll
+            for (int e = 0; e < 9; ++e) sg.a[e] = 0.0;
+            const double inv = 1.0 / mass;
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+#pragma unroll
+              for (int b = a; b < D; ++b) sg(a, b) = S.st2[i][1 + D + uidx<D>(a, b)] * inv;
+            symmetrize_from_upper<D>(sg);
+            certified = lmin_lower_bound<D>(sg) > 1e-14 * trace3<D>(sg);
+          } else {
+            load_cov<D>(S.sig1[i], sg);
+            certified = (S.cert_mask >> i) & 1;
+          }
+#pragma unroll
+          for (int a = 0; a < D; ++a) S.mu[i][a] = S.mu_new[i][a];
+          Sym3 acc;
+          if (certified) {
+#pragma unroll
+            for (int e = 0; e < 9; ++e) S.cov[i][e] = sg.a[e];
+          } else if (accept_covariance<D>(sg, acc)) {
+#pragma unroll
+            for (int e = 0; e < 9; ++e) S.cov[i][e] = acc.a[e];
+          } else {
+            degen = true;
+          }
+        }
+      }
+      const unsigned gm = __ballot_sync(0xffffffffu, degen);
+      if (lane == 0) S.degen_mask = static_cast<int>(gm);
+    }
+    __syncthreads();
+
+    // ---- protocol: removal, pruning, convergence (wgmm.cpp:383-417), thread 0
+    if (threadIdx.x == 0) {
+      const double ll = S.ll;
+      if (out.trace && it - 1 < out.trace_cap)
+        out.trace[static_cast<int64_t>(c) * out.trace_cap + (it - 1)] = ll;
+      const int mask = S.dead_mask | S.degen_mask;
+      bool pruned = false;
+      for (int i = S.m - 1; i >= 0; --i) {
+        if (!((mask >> i) & 1)) continue;
+        if (S.m <= 1) break;
+        if (out.ev_it && S.n_events < out.K) {
+          const int64_t e = static_cast<int64_t>(c) * out.K + S.n_events;
+          out.ev_it[e] = it;
+          out.ev_comp[e] = i;
+          out.ev_w[e] = S.alpha[i];
+        }
+        ++S.n_events;
+        remove_component<D>(S.alpha, &S.mu[0][0], &S.cov[0][0], S.m, i);
+        pruned = true;
+      }
+      if (pruned) renormalize(S.alpha, S.m);
+      if (it % cfg.interval == 0) {  // prune_one, wgmm.cpp:320-333
+        int idx = -1;
+        double wgt = 0.0;
+        if (prune_one_dev<D>(S.alpha, &S.mu[0][0], &S.cov[0][0], S.m, cfg.prune_thr, &idx, &wgt)) {
+          if (out.ev_it && S.n_events < out.K) {
+            const int64_t e = static_cast<int64_t>(c) * out.K + S.n_events;
+            out.ev_it[e] = it;
+            out.ev_comp[e] = idx;
+            out.ev_w[e] = wgt;
+          }
+          ++S.n_events;
+          pruned = true;
+        }
+      }
+      S.it_used = it;
+      if (!pruned && isfinite(S.prev_ll) && fabs(ll - S.prev_ll) < cfg.tol * fabs(S.prev_ll)) {
+        S.converged = 1;
+        S.stop = 1;
+      }
+      S.prev_ll = pruned ? dnan() : ll;
+    }
+    __syncthreads();
+    if (S.stop) break;
+  }
+
+  // ---- epilogue: denormalize (wgmm.cpp:102-120) and write
+  const int K_out = out.K;
+  const int64_t base = static_cast<int64_t>(c) * K_out;
+  if (S.status == 0) {
+    bool ident = true;
+#pragma unroll
+    for (int a = 0; a < D; ++a) ident = ident && S.fr.scale[a] == 1.0 && S.fr.offset[a] == 0.0;
+    for (int i = threadIdx.x; i < S.m; i += blockDim.x) {
+      out.w[base + i] = S.alpha[i];
+      Sym3 cv;
+      load_cov<D>(S.cov[i], cv);
+      if (!ident) {
+        Sym3 t;
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+          for (int b = 0; b < D; ++b)
+            t(a, b) = __dmul_rn(__dmul_rn(S.fr.scale[a], cv(a, b)), S.fr.scale[b]);
+        symmetrize_from_upper<D>(t);
+        cv = t;
+      }
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const double v = ident ? S.mu[i][a] : __dadd_rn(__dmul_rn(S.mu[i][a], S.fr.scale[a]), S.fr.offset[a]);
+        out.mu[(base + i) * D + a] = v;
+#pragma unroll
+        for (int b = 0; b < D; ++b) out.cov[((base + i) * D + a) * D + b] = cv(a, b);
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
+    out.status[c] = S.status;
+    out.comps[c] = S.status ? 0 : S.m;
+    out.iters[c] = S.status ? 0 : min(S.it_used, cfg.max_it);
+    out.conv[c] = S.status ? 0 : S.converged;
+    out.final_ll[c] = S.status ? dnan() : S.ll;
+    if (out.n_events) out.n_events[c] = S.status ? 0 : min(S.n_events, K_out);
+    if (out.err_axis) out.err_axis[c] = S.status ? S.err_id : -1;
+    if (out.err_value) out.err_value[c] = S.fr.err_value;
+  }
+  (void)NS;
+}
+
+// ---------------------------------------------------------------- prologues
+// Histogram-derived cell: normalize over the occupied bins, z tables, temperature.
+template <int D, int K>
+VDFCG_DEV int key_prologue(const KeyCells& kc, int c, const EmConfig& cfg, EmState<D, K>& S,
+                           double* ztab, double* red, KeySrc<D>& src) {
+  const int nb = kc.n_bins;
+  const int64_t base = kc.offsets[c];
+  const int n = kc.nnz[c];
+  src.keys = kc.keys + base;
+  src.counts = kc.counts + base;
+  src.nb = nb;
+  src.packed = kc.packed + base;
+  src.ztab = ztab;
+  if (threadIdx.x == 0) {
+    S.status = 0;
+    S.err_id = -1;
+    S.fr.err_value = 0.0;
+    for (int a = 0; a < 3; ++a) {
+      S.minidx[a] = nb;
+      S.maxidx[a] = -1;
+    }
+  }
+  __syncthreads();
+  const bool need_temp = !cfg.has_temp && cfg.warm_m == 0;
+  double sw = 0.0, sx[3] = {0, 0, 0}, sxx[3] = {0, 0, 0};
+  int mn[3] = {nb, nb, nb}, mxi[3] = {-1, -1, -1};
+  for (int p = threadIdx.x; p < n; p += blockDim.x) {
+    uint32_t k = __ldg(src.keys + p);
+    int idx[3];
+#pragma unroll
+    for (int a = D - 1; a >= 0; --a) {
+      const uint32_t q = k / static_cast<uint32_t>(nb);
+      idx[a] = static_cast<int>(k - q * static_cast<uint32_t>(nb));
+      k = q;
+    }
+    {
+      uint32_t pk = 0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) pk |= static_cast<uint32_t>(idx[a]) << (KeySrc<D>::SHIFT * a);
+      src.packed[p] = pk;
+    }
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      mn[a] = min(mn[a], idx[a]);
+      mxi[a] = max(mxi[a], idx[a]);
+    }
+    if (need_temp) {
+      const double w = __ldg(src.counts + p);
+      sw += w;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const double x = bin_center(kc.lo[a], kc.hi[a], nb, idx[a]);
+        const double xw = x * w;
+        sx[a] += xw;
+        sxx[a] += xw * x;
+      }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    mn[a] = warp_min(mn[a]);
+    mxi[a] = warp_max(mxi[a]);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, G = blockDim.x >> 5;
+  if (lane == 0) {
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      atomicMin(&S.minidx[a], mn[a]);
+      atomicMax(&S.maxidx[a], mxi[a]);
+    }
+  }
+  if (need_temp) {
+    sw = warp_sum(sw);
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      sx[a] = warp_sum(sx[a]);
+      sxx[a] = warp_sum(sxx[a]);
+    }
+    if (lane == 0) {
+      red[warp * 8 + 0] = sw;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        red[warp * 8 + 1 + a] = sx[a];
+        red[warp * 8 + 4 + a] = sxx[a];
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Frame& F = S.fr;
+    const double total = kc.in_range[c];
+    F.total = total;
+    F.status = 0;
+    if (n <= 0 || !(total > 0.0)) {
+      S.status = VDFCG_INVALID_ARGUMENT;
+      S.err_id = kMsgDegenerateHist;
+    } else {
+      for (int a = 0; a < D; ++a) {
+        const double lo = bin_center(kc.lo[a], kc.hi[a], nb, S.minidx[a]);
+        const double hi = bin_center(kc.lo[a], kc.hi[a], nb, S.maxidx[a]);
+        F.offset[a] = __dmul_rn(0.5, __dadd_rn(lo, hi));
+        F.scale[a] = __dmul_rn(0.5, __dsub_rn(hi, lo));
+      }
+      for (int a = 0; a < D; ++a) {
+        if (!(F.scale[a] > 0.0)) {
+          S.status = VDFCG_INVALID_ARGUMENT;
+          S.err_id = kMsgZeroSpread + a;
+          F.err_value = bin_center(kc.lo[a], kc.hi[a], nb, S.minidx[a]);
+          break;
+        }
+      }
+      if (!S.status) {
+        if (cfg.has_temp) {
+          for (int a = 0; a < D; ++a) F.temp[a] = cfg.temp[a];
+        } else if (cfg.warm_m == 0) {
+          double tsw = 0.0, tsx[3] = {0, 0, 0}, tsxx[3] = {0, 0, 0};
+          for (int g = 0; g < G; ++g) {
+            tsw += red[g * 8];
+            for (int a = 0; a < D; ++a) {
+              tsx[a] += red[g * 8 + 1 + a];
+              tsxx[a] += red[g * 8 + 4 + a];
+            }
+          }
+          for (int a = 0; a < D; ++a) {
+            const double mean = tsx[a] / tsw;
+            const double var = fmax(tsxx[a] / tsw - mean * mean, 0.0);
+            F.temp[a] = var;
+            if (!(var > 0.0)) {
+              S.status = VDFCG_INVALID_ARGUMENT;
+              S.err_id = kMsgTemperature;
+            }
+          }
+        }
+        F.m_init = min(cfg.M, n);  // bin centres are distinct points (wgmm.cpp:166-172)
+      }
+    }
+  }
+  __syncthreads();
+  if (S.status) return n;
+  for (int t = threadIdx.x; t < D * nb; t += blockDim.x) {
+    const int a = t / nb, i = t - a * nb;
+    ztab[t] = __dsub_rn(bin_center(kc.lo[a], kc.hi[a], nb, i), S.fr.offset[a]) / S.fr.scale[a];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int a = 0; a < D; ++a) {
+      S.fr.zlo[a] = ztab[a * nb + S.minidx[a]];
+      S.fr.zhi[a] = ztab[a * nb + S.maxidx[a]];
+    }
+  }
+  __syncthreads();
+  return n;
+}
+
+template <int D, int K, bool KEYS>
+__global__ void __launch_bounds__(256, (K <= 4 ? 2 : 1)) em_kernel(KeyCells kc, CoordArgs ca, EmConfig cfg,
+                                                 EmOut out, int* counter, int red_stride) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  EmState<D, K>& S = *reinterpret_cast<EmState<D, K>*>(smem_raw);
+  constexpr size_t st_bytes = (sizeof(EmState<D, K>) + 15) & ~size_t(15);
+  double* red = reinterpret_cast<double*>(smem_raw + st_bytes);
+  double* ztab = red + (blockDim.x >> 5) * red_stride;
+  const int n_cells = KEYS ? kc.n_cells : 1;
+  for (int j = threadIdx.x; j < 64; j += blockDim.x) S.exp2tab[j] = kExp2Tab[j];
+  for (;;) {
+    if (threadIdx.x == 0) S.cell = atomicAdd(counter, 1);
+    __syncthreads();
+    const int c = S.cell;
+    if (c >= n_cells) break;
+    if (KEYS) {
+      KeySrc<D> src;
+      const int n = key_prologue<D, K>(kc, c, cfg, S, ztab, red, src);
+      run_fit<D, K>(src, n, S, red, cfg, out, c);
+    } else {
+      if (threadIdx.x == 0) {
+        S.fr = *ca.frame;
+        S.status = S.fr.status;
+        S.err_id = S.fr.err_axis;
+      }
+      __syncthreads();
+      CoordSrc<D> src{ca.z, ca.n, ca.w};
+      if (S.status) {
+        if (threadIdx.x == 0) {
+          out.status[c] = S.status;
+          out.comps[c] = 0;
+          out.iters[c] = 0;
+          out.conv[c] = 0;
+          out.final_ll[c] = dnan();
+          if (out.n_events) out.n_events[c] = 0;
+          if (out.err_axis) out.err_axis[c] = S.err_id;
+          if (out.err_value) out.err_value[c] = S.fr.err_value;
+        }
+      } else {
+        run_fit<D, K>(src, static_cast<int>(ca.n), S, red, cfg, out, c);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- host launch
+template <int D, int K, bool KEYS>
+void launch_em_t(vdfcg_ctx* ctx, const KeyCells& kc, const CoordArgs& ca,
+                        const EmConfig& cfg, const EmOut& out, int n_cells, int G, int n_bins) {
+  constexpr int NS = NStat<D>::value;
+  const int red_stride = std::max(K * NS + 1, 8);
+  const size_t st = (sizeof(EmState<D, K>) + 15) & ~size_t(15);
+  const size_t smem = st + size_t(G) * red_stride * 8 + (KEYS ? size_t(D) * n_bins * 8 : 0);
+  auto k = em_kernel<D, K, KEYS>;
+  VDFCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int occ = 0;
+  VDFCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, G * 32, smem));
+  if (occ < 1) throw CudaError("EM kernel cannot be resident (registers/shared memory)");
+  const int grid = std::max(1, std::min(n_cells, ctx->sm_count * occ));
+  int* counter = arena<int>(ctx, 1);
+  VDFCG_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), ctx->stream));
+  VDFCG_LAUNCH(ctx, "em_fit",
+               k<<<grid, G * 32, smem, ctx->stream>>>(kc, ca, cfg, out, counter, red_stride));
+}
+
+template <int D, bool KEYS>
+void launch_em_k(vdfcg_ctx* ctx, int K, const KeyCells& kc, const CoordArgs& ca,
+                 const EmConfig& cfg, const EmOut& out, int n_cells, int G, int n_bins) {
+  switch (K) {  // exact capacities for the common sizes, next larger otherwise
+    case 1: launch_em_t<D, 1, KEYS>(ctx, kc, ca, cfg, out, n_cells, G, n_bins); break;
+    case 2: launch_em_t<D, 2, KEYS>(ctx, kc, ca, cfg, out, n_cells, G, n_bins); break;
+    case 3: launch_em_t<D, 3, KEYS>(ctx, kc, ca, cfg, out, n_cells, G, n_bins); break;
+    case 4: launch_em_t<D, 4, KEYS>(ctx, kc, ca, cfg, out, n_cells, G, n_bins); break;
+    case 5: launch_em_t<D, 5, KEYS>(ctx, kc, ca, cfg, out, n_cells, G, n_bins); break;
+    case 6: launch_em_t<D, 6, KEYS>(ctx, kc, ca, cfg, out, n_cells, G, n_bins); break;
+    case 7:
+    case 8: launch_em_t<D, 8, KEYS>(ctx, kc, ca, cfg, out, n_cells, G, n_bins); break;
+    case 9: case 10: case 11:
+    case 12: launch_em_t<D, 12, KEYS>(ctx, kc, ca, cfg, out, n_cells, G, n_bins); break;
+    default: launch_em_t<D, 16, KEYS>(ctx, kc, ca, cfg, out, n_cells, G, n_bins); break;
+  }
+}
+
+// Warps per fit: enough lanes that each holds ~16 points per pass, and enough CTAs in
+// flight to fill every SM; deterministic in the input shape only.
+
+}  // namespace vdfcg
