@@ -12,6 +12,7 @@
 #include <array>
 #include <atomic>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <limits>
 #include <random>
@@ -271,9 +272,11 @@ void normalize_impl(const Points& p, Points& out, double* scale, double* offset)
   }
   for (int a = 0; a < d; ++a) {
     if (!(scale[a] > 0.0)) {
-      std::ostringstream msg;
-      msg << "degenerate data: axis " << a << " has zero spread (all values " << lo[a] << ")";
-      throw std::invalid_argument(msg.str());
+      // std::ostream default formatting of a double == %g (6 significant digits)
+      char msg[160];
+      std::snprintf(msg, sizeof(msg), "degenerate data: axis %d has zero spread (all values %g)", a,
+                    lo[a]);
+      throw std::invalid_argument(msg);
     }
   }
   out = p;

@@ -1,0 +1,157 @@
+"""GPU: golden vectors produced by the reference's own refem::fit, full-size BASELINE
+configs against the oracle, bitwise determinism, and size-independent properties at
+full cfg4 scale (mass conservation, unit weight sums, record integrity)."""
+import glob
+import os
+import struct
+import zlib
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2504_14897_b200 as G
+from helpers import TOL_EM, model_close
+from paper_2504_14897_b200.types import (AffineMap, AxisRange, FitConfig, GaussianComponent,
+                                         GmmModel, ModelMeta, WeightedPoints)
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _rel(a, b):
+    return np.max(np.abs(np.asarray(a) - np.asarray(b)) / np.maximum(np.maximum(np.abs(a), np.abs(b)), 1.0))
+
+
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLD, "refem_*.npz"))))
+def test_gpu_fit_matches_reference_refem(path):
+    """Acceptance criterion 5 against the reference's own EM (golden outputs)."""
+    g = np.load(path)
+    wp = WeightedPoints.from_(np.stack([g["xs"], g["ys"]], 1), np.ones(len(g["xs"])))
+    r = G.fit(wp, FitConfig(initial_components=int(g["m"]), seed=int(g["seed"]), temperature=np.ones(2)))
+    assert r.iterations_used == int(g["iterations"]) and r.model.size() == len(g["alpha"])
+    for i, c in enumerate(r.model.components):
+        assert _rel(c.weight, g["alpha"][i]) <= TOL_EM
+        assert _rel(c.mean, g["means"][i]) <= TOL_EM
+        assert _rel(c.covariance, g["covs"][i]) <= TOL_EM
+    assert _rel(r.loglik_trace, g["trace"]) <= TOL_EM
+
+
+def _batch(v, offs, nb, r, w=None):
+    d = v.shape[1]
+    return G.CellBatch([np.ascontiguousarray(v[:, a]) for a in range(d)], offs, nb, [-r] * d, [r] * d, w)
+
+
+def _oracle_model(res, c, d):
+    k = res.k
+    comps = [GaussianComponent(res.weights[c * k + i], res.means[(c * k + i) * d:(c * k + i + 1) * d],
+                               res.covariances[(c * k + i) * d * d:(c * k + i + 1) * d * d].reshape(d, d))
+             for i in range(res.components[c])]
+    return GmmModel(comps, AffineMap.identity(d), d)
+
+
+def test_cfg2_full_size_parity():
+    """BASELINE cfg2: one cell, 1e7 particles, 3V 32^3 bins, K=4 full covariances."""
+    covs = []
+    rng = np.random.default_rng(7)
+    for k in range(4):
+        a = np.eye(3) + 0.3 * (np.ones((3, 3)) - np.eye(3))
+        covs.append(a * rng.uniform(0.3, 1.0))
+    p = O.generate([0.4, 0.3, 0.2, 0.1], [[0, 0, 0], [2.5, 0, 0], [-1.5, 1.5, 0], [0, -2, 1.5]],
+                   covs, 10_000_000, 17)
+    offs = np.array([0, p.count()], dtype=np.int64)
+    cfg = FitConfig(initial_components=4, seed=17, temperature=p.nominal_temperature)
+    ob, orr = O.compress_cells(O.CellsHost(p.velocities, offs, 32, [-6] * 3, [6] * 3), cfg,
+                               trace=cfg.max_em_iterations)
+    gb, gr, _, _ = G.compress_cells(_batch(p.velocities, offs, 32, 6.0), cfg, trace=True)
+    assert np.array_equal(gb.nnz, ob.nnz)
+    k = int(ob.nnz[0])
+    assert np.array_equal(gb.keys[:k], ob.keys[:k]) and np.array_equal(gb.counts[:k], ob.counts[:k])
+    assert gr.status[0] == 0 and gr.iterations[0] == orr.iterations[0]
+    assert gr.components[0] == orr.components[0]
+    n_it = int(orr.iterations[0])
+    assert _rel(gr.loglik_trace[:n_it], orr.loglik_trace[:n_it]) <= TOL_EM
+    assert model_close(gr.model(0), _oracle_model(orr, 0, 3)) <= TOL_EM
+
+
+def test_cfg1_full_size_all_planes_and_fit():
+    p = O.preset("drifting-beam", 1_000_000, 11)
+    hg = G.all_planes(p, 64, AxisRange(-6, 6))
+    ho = O.all_planes(p, 64, AxisRange(-6, 6))
+    cfg = FitConfig(initial_components=2, seed=11, temperature=np.ones(2))
+    for a, b in zip(hg, ho):
+        assert np.array_equal(a.counts, b.counts)
+        rg, ro = G.fit(G.to_weighted_points(a), cfg), O.fit(O.to_weighted_points(b), cfg)
+        assert rg.iterations_used == ro.iterations_used and model_close(rg.model, ro.model) <= TOL_EM
+
+
+def test_weighted_cells_parity():
+    rng = np.random.default_rng(4)
+    offs = np.arange(33, dtype=np.int64) * 1500
+    v = rng.normal(size=(int(offs[-1]), 3))
+    w = rng.uniform(0.1, 4.0, size=int(offs[-1]))
+    cfg = FitConfig(initial_components=3, seed=5, temperature=np.ones(3))
+    ob, orr = O.compress_cells(O.CellsHost(v, offs, 48, [-5] * 3, [5] * 3, w), cfg)
+    gb, gr, _, _ = G.compress_cells(_batch(v, offs, 48, 5.0, w), cfg)
+    for c in range(32):
+        b, k = offs[c], ob.nnz[c]
+        assert np.array_equal(gb.counts[b:b + k], ob.counts[b:b + k])  # sequential sums: bit-exact
+    assert np.array_equal(gr.iterations, orr.iterations)
+    for c in range(32):
+        assert model_close(gr.model(c), _oracle_model(orr, c, 3)) <= TOL_EM
+
+
+def test_determinism_bitwise():
+    import torch
+    dev = torch.device("cuda", 0)
+    offs = torch.arange(2049, dtype=torch.int64, device=dev) * 1900
+    axes = [torch.empty(2048 * 1900, dtype=torch.float64, device=dev) for _ in range(3)]
+    G.synth_cells(3, offs, 11, 0, *axes)
+    b = G.CellBatch(axes, offs, 48, [-6] * 3, [6] * 3)
+    cfg = FitConfig(initial_components=4, seed=11, temperature=np.ones(3))
+    meta = ModelMeta("e", None, 0, [AxisRange(-6, 6)] * 3)
+    _, r1, rec1, _ = G.compress_cells(b, cfg, meta)
+    _, r2, rec2, _ = G.compress_cells(b, cfg, meta)
+    assert torch.equal(rec1, rec2)
+    for f in ("weights", "means", "covariances", "final_loglik", "iterations"):
+        assert torch.equal(getattr(r1, f), getattr(r2, f))
+
+
+def test_cfg4_scale_properties():
+    """One cfg4 species at full scale on one GPU (262144 cells, 5e8 particles): exact mass
+    conservation per cell, every fit valid (status 0, weights sum to 1 within 1e-12,
+    SPD covariances), every .gmmc record well formed (magic, CRC, size)."""
+    import torch
+    dev = torch.device("cuda", 0)
+    n_cells, total = 64 ** 3, 500_000_000
+    base, extra = divmod(total, n_cells)
+    counts = np.full(n_cells, base, dtype=np.int64)
+    counts[:extra] += 1
+    offs_h = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    offs = torch.from_numpy(offs_h).to(dev)
+    axes = [torch.empty(total, dtype=torch.float64, device=dev) for _ in range(3)]
+    G.synth_cells(3, offs, 11, 0, *axes)
+    b = G.CellBatch(axes, offs, 48, [-6] * 3, [6] * 3)
+    cfg = FitConfig(initial_components=4, seed=11, temperature=np.ones(3))
+    bins, res, rec, roffs = G.compress_cells(b, cfg, ModelMeta("e", None, 0, [AxisRange(-6, 6)] * 3))
+    tot = (bins.in_range + bins.out_of_range).cpu().numpy()
+    assert np.array_equal(tot, counts.astype(np.float64))
+    st = res.status.cpu().numpy()
+    assert (st == 0).all()
+    K = res.k
+    m = res.components.cpu().numpy()
+    w = res.weights.cpu().numpy().reshape(n_cells, K)
+    mask = np.arange(K)[None, :] < m[:, None]
+    assert np.abs((w * mask).sum(1) - 1.0).max() <= 1e-12
+    cov = res.covariances.cpu().numpy().reshape(n_cells, K, 3, 3)
+    ev = np.linalg.eigvalsh(cov[mask])
+    assert (ev > 0).all()
+    rec_h = rec.cpu().numpy().tobytes()
+    ro = roffs.cpu().numpy()
+    for c in np.random.default_rng(0).choice(n_cells, 2000, replace=False):
+        r = rec_h[ro[c]:ro[c + 1]]
+        assert r[:4] == b"GMMC" and r[5] == 3
+        hb = 26 + 16 * 3 + 1
+        assert struct.unpack("<I", r[hb - 4:hb])[0] == zlib.crc32(r[:hb - 4])
+        assert len(r) == hb + m[c] * 80
+        assert struct.unpack("<I", r[8:12])[0] == m[c]
