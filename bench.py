@@ -26,6 +26,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+ORACLE_DIR = os.path.join(ROOT, "oracle")  # CPU baseline / reference arm only
 
 # workload definitions (BASELINE.json configs)
 CONFIGS = {
@@ -190,6 +191,8 @@ def sample_cells(cfg, n_sample_cells_per_species):
 def cpu_oracle_rate(cfg, cells_per_species, threads, gpu_results=None):
     """Time the CPU oracle (bin + compact + fit per cell, pipeline.cpp:140-151) on a
     bounded sample; returns (particles/s, fits/s, seconds, particles, fits, parity)."""
+    if ORACLE_DIR not in sys.path:
+        sys.path.insert(0, ORACLE_DIR)
     import oracle as O
     from paper_2504_14897_b200.types import FitConfig
     counts = cell_counts(cfg)

@@ -461,7 +461,7 @@ struct Kahan {  // gaussian.hpp:55-68
 double e_step_impl(Model& m, const Points& p, std::vector<double>& resp,
                    std::vector<int>& unrepairable) {
   const int M = static_cast<int>(m.c.size());
-  std::vector<double> logp;
+  thread_local std::vector<double> logp;  // reused across iterations (capacity kept)
   log_component_densities(m, p, logp, &unrepairable);
   if (static_cast<int>(unrepairable.size()) == M)
     throw std::runtime_error("all mixture components are degenerate");
@@ -506,7 +506,8 @@ Model m_step_impl(const Points& p, double total, const std::vector<double>& resp
   std::memcpy(out.scale, prev.scale, sizeof(out.scale));
   std::memcpy(out.offset, prev.offset, sizeof(out.offset));
   out.c.resize(M);
-  std::vector<double> wi(p.n);
+  thread_local std::vector<double> wi;
+  wi.resize(p.n);
   for (int i = 0; i < M; ++i) {
     Comp& c = out.c[i];
     c.w = mass[i] / total;
@@ -516,19 +517,21 @@ Model m_step_impl(const Points& p, double total, const std::vector<double>& resp
       continue;
     }
     for (int64_t n = 0; n < p.n; ++n) wi[n] = resp[i + n * M] * p.w[n];
-    for (int a = 0; a < d; ++a) {
-      double s = 0.0;
-      for (int64_t n = 0; n < p.n; ++n) s += p.at(n, a) * wi[n];
-      c.mu[a] = s / mass[i];
-    }
+    // one pass per moment order; every entry keeps the sequential order over n
+    double sm[3] = {0.0, 0.0, 0.0};
+    for (int64_t n = 0; n < p.n; ++n)
+      for (int a = 0; a < d; ++a) sm[a] += p.at(n, a) * wi[n];
+    for (int a = 0; a < d; ++a) c.mu[a] = sm[a] / mass[i];
     Mat3 sigma{};
+    double ss[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    for (int64_t n = 0; n < p.n; ++n) {
+      double cen[3];
+      for (int a = 0; a < d; ++a) cen[a] = p.at(n, a) - c.mu[a];
+      for (int a = 0; a < d; ++a)
+        for (int b = a; b < d; ++b) ss[a][b] += (cen[a] * wi[n]) * cen[b];
+    }
     for (int a = 0; a < d; ++a)
-      for (int b = a; b < d; ++b) {
-        double s = 0.0;
-        for (int64_t n = 0; n < p.n; ++n)
-          s += ((p.at(n, a) - c.mu[a]) * wi[n]) * (p.at(n, b) - c.mu[b]);
-        sigma[a][b] = s / mass[i];
-      }
+      for (int b = a; b < d; ++b) sigma[a][b] = ss[a][b] / mass[i];
     symmetrize_from_upper(sigma, d);
     bool collapsed = false;
     bool finite = true;
@@ -633,9 +636,10 @@ FitOut fit_impl(const Points& pts, const vdfcg_fit_config* cfg) {
   FitOut r;
   double prev_ll = kNaN;
   int it = 0;
+  std::vector<double> resp;
+  std::vector<int> unrep;
   for (it = 1; it <= cfg->max_em_iterations; ++it) {
-    std::vector<double> resp;
-    std::vector<int> unrep;
+    unrep.clear();
     const double ll = e_step_impl(model, np, resp, unrep);
     std::vector<int> degenerate = unrep;
     model = m_step_impl(np, np.total, resp, model, &degenerate);

@@ -340,17 +340,28 @@ __global__ void __launch_bounds__(1024) cells_dense_kernel(
     unsigned long long oor = 0;
     double ow = 0.0;
     bool bad = false;
-    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
-      const int64_t key = cell_key<D>(vp.v, i, g);
-      if (weighted) {
-        const double wt = __ldg(w + i);
-        bad |= !(wt > 0.0);
-        if (key < 0) ow += wt;
-        else atomicAdd(densew + static_cast<int64_t>(c) * bins + key, wt);
-      } else {
-        if (key < 0) ++oor;
-        else if (SMEM) atomicAdd(sh + key, 1u);
-        else atomicAdd(dense + static_cast<int64_t>(c) * bins + key, 1u);
+    constexpr int U = 4;  // 4 particles per thread in flight: 12 independent 8-byte loads
+    for (int64_t i0 = b + threadIdx.x; i0 < e; i0 += int64_t(U) * blockDim.x) {
+      int64_t key[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + int64_t(u) * blockDim.x;
+        key[u] = i < e ? cell_key<D>(vp.v, i, g) : -2;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + int64_t(u) * blockDim.x;
+        if (key[u] == -2) continue;
+        if (weighted) {
+          const double wt = __ldg(w + i);
+          bad |= !(wt > 0.0);
+          if (key[u] < 0) ow += wt;
+          else atomicAdd(densew + static_cast<int64_t>(c) * bins + key[u], wt);
+        } else {
+          if (key[u] < 0) ++oor;
+          else if (SMEM) atomicAdd(sh + key[u], 1u);
+          else atomicAdd(dense + static_cast<int64_t>(c) * bins + key[u], 1u);
+        }
       }
     }
     if (bad) atomicOr(err, 1);
@@ -428,6 +439,9 @@ __global__ void __launch_bounds__(512) cells_compact_kernel(
 }
 
 // K3: per-cell composite-key sort. key = (bin << IDXB) | local index; OOR bin = SENT.
+// Unit weights sort the bin key alone (counts = run lengths; order within a run is
+// irrelevant); fractional weights sort (bin, particle) so each run is summed in particle
+// order. 6-bit digits: 3 passes for 48^3 / 64^3 bins on the unit-weight path.
 template <int D, int BLOCK, int IPT, bool W>
 __global__ void __launch_bounds__(BLOCK) cells_sort_kernel(
     VelPtrs vp, const double* __restrict__ w, const int64_t* __restrict__ offsets, int n_cells,
@@ -457,15 +471,15 @@ __global__ void __launch_bounds__(BLOCK) cells_sort_kernel(
       if (li < nc) {
         const int64_t key = cell_key<D>(vp.v, b + li, g);
         const uint32_t bin = key < 0 ? sent : static_cast<uint32_t>(key);
-        k[i] = (bin << idxbits) | static_cast<uint32_t>(li);
+        k[i] = W ? ((bin << idxbits) | static_cast<uint32_t>(li)) : bin;
         if (W) bad |= !(__ldg(w + b + li) > 0.0);
       } else {
-        k[i] = 0xffffffffu;
+        k[i] = W ? 0xffffffffu : sent;  // padding sorts with (after) the out-of-range keys
       }
     }
     if (W && bad) atomicOr(err, 1);
     __syncthreads();
-    Sort(sort_ts).Sort(k, 0, binbits + idxbits);
+    Sort(sort_ts).Sort(k, 0, binbits + (W ? idxbits : 0));
     __syncthreads();
     // blocked arrangement: thread t holds sorted positions t*IPT + i
 #pragma unroll
@@ -538,6 +552,104 @@ __global__ void __launch_bounds__(BLOCK) cells_sort_kernel(
   }
 }
 
+// K3b: sparse unit-weight cells without sorting. A shared-memory occupancy bitmap over
+// the cell's bins^d grid (1 bit per bin), a block prefix of per-word popcounts gives
+// every occupied bin its rank in ascending key order (= to_weighted_points order), a
+// second pass counts particles per rank, and set bits are emitted in order. Cost per
+// cell: bins/32 words + 2 shared atomics per particle; particles are read once.
+template <int D, int BLOCK>
+__global__ void __launch_bounds__(BLOCK) cells_bitmap_kernel(
+    VelPtrs vp, const int64_t* __restrict__ offsets, int n_cells, CellGeom g, int words, int ccap,
+    int cap, int32_t* nnz, uint32_t* __restrict__ keys_out, double* __restrict__ counts_out,
+    double* oor_out, double* in_range) {
+  using Scan = cub::BlockScan<unsigned, BLOCK>;
+  using Reduce = cub::BlockReduce<unsigned, BLOCK>;
+  __shared__ typename Scan::TempStorage ss;
+  __shared__ typename Reduce::TempStorage rs;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned* bitmap = reinterpret_cast<unsigned*>(smem_raw);  // [words]
+  unsigned* wpre = bitmap + words;                           // [words] exclusive prefix
+  unsigned* cnt = wpre + words;                              // [ccap >= max nnz] per-rank counts
+  unsigned* kbuf = cnt + ccap;                               // [cap] keys of this cell
+  const int wpt = (words + BLOCK - 1) / BLOCK;
+  for (int c = blockIdx.x; c < n_cells; c += gridDim.x) {
+    const int64_t b = offsets[c];
+    const int nc = static_cast<int>(offsets[c + 1] - b);
+    for (int t = threadIdx.x; t < words; t += BLOCK) bitmap[t] = 0u;
+    for (int t = threadIdx.x; t < min(nc, ccap); t += BLOCK) cnt[t] = 0u;
+    __syncthreads();
+    unsigned oor = 0;
+    constexpr int U = 8;  // 8 particles (24 independent 8-byte loads) in flight per thread
+    for (int l0 = threadIdx.x; l0 < nc; l0 += U * BLOCK) {
+      int64_t key[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int li = l0 + u * BLOCK;
+        key[u] = li < nc ? cell_key<D>(vp.v, b + li, g) : -2;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int li = l0 + u * BLOCK;
+        if (key[u] == -2) continue;
+        if (key[u] < 0) ++oor;
+        else atomicOr(bitmap + (key[u] >> 5), 1u << (key[u] & 31));
+        if (li < cap) kbuf[li] = key[u] < 0 ? 0xffffffffu : static_cast<unsigned>(key[u]);
+      }
+    }
+    __syncthreads();
+    unsigned local = 0;
+    for (int k = 0; k < wpt; ++k) {
+      const int wi = threadIdx.x * wpt + k;
+      if (wi < words) local += __popc(bitmap[wi]);
+    }
+    unsigned pre, total;
+    Scan(ss).ExclusiveSum(local, pre, total);
+    for (int k = 0; k < wpt; ++k) {
+      const int wi = threadIdx.x * wpt + k;
+      if (wi < words) {
+        wpre[wi] = pre;
+        pre += __popc(bitmap[wi]);
+      }
+    }
+    __syncthreads();
+    for (int li = threadIdx.x; li < nc; li += BLOCK) {
+      unsigned key;
+      if (li < cap) {
+        key = kbuf[li];
+      } else {
+        const int64_t k2 = cell_key<D>(vp.v, b + li, g);
+        key = k2 < 0 ? 0xffffffffu : static_cast<unsigned>(k2);
+      }
+      if (key != 0xffffffffu) {
+        const unsigned wd = key >> 5, bit = key & 31;
+        const unsigned r = wpre[wd] + __popc(bitmap[wd] & ((1u << bit) - 1u));
+        atomicAdd(cnt + r, 1u);
+      }
+    }
+    __syncthreads();
+    for (int k = 0; k < wpt; ++k) {
+      const int wi = threadIdx.x * wpt + k;
+      if (wi >= words) break;
+      unsigned bits = bitmap[wi];
+      unsigned r = wpre[wi];
+      while (bits) {
+        const unsigned bit = __ffs(bits) - 1;
+        keys_out[b + r] = (static_cast<unsigned>(wi) << 5) | bit;
+        counts_out[b + r] = static_cast<double>(cnt[r]);
+        ++r;
+        bits &= bits - 1;
+      }
+    }
+    const unsigned to = Reduce(rs).Sum(oor);
+    if (threadIdx.x == 0) {
+      nnz[c] = static_cast<int32_t>(total);
+      oor_out[c] = static_cast<double>(to);
+      in_range[c] = static_cast<double>(nc - static_cast<int>(to));
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void chunks_per_cell_kernel(const int64_t* offsets, int n_cells, int64_t chunk,
                                        int64_t* out) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n_cells; c += gridDim.x * blockDim.x) {
@@ -603,7 +715,7 @@ static void launch_sort(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
   int occ = 0;
   VDFCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, BLOCK, smem));
   const int grid = std::max(1, std::min(c.n_cells, ctx->sm_count * std::max(occ, 1)));
-  int idxbits = bits_for(CAP - 1);
+  const int idxbits = W ? bits_for(CAP - 1) : 0;
   VelPtrs vp{{c.vel[0], c.vel[1], c.vel[2]}};
   VDFCG_LAUNCH(ctx, "cells_sort",
                k<<<grid, BLOCK, smem, ctx->stream>>>(vp, c.w, c.offsets, c.n_cells, g, binbits,
@@ -640,9 +752,29 @@ static void bin_cells_d(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
   const int64_t maxc = max_cell_size(ctx, c.offsets, c.n_cells);
   const double avg = c.n_cells ? double(c.n) / c.n_cells : 0.0;
   const int binbits = bits_for(static_cast<uint64_t>(bins));  // SENT = 2^binbits - 1 > any bin
-  // Sparse cells (or fractional weights, which the sort path sums bit-exactly): sort.
+  // Sparse cells: unit weights use the occupancy bitmap (no sort); fractional weights
+  // use the composite-key sort, which sums every bin in particle order (bit-exact).
   bool done = false;
-  if (maxc <= 8192 && (weighted || avg * 4.0 < double(bins) || maxc <= 1024)) {
+  const bool sparse = avg * 4.0 < double(bins) || maxc <= 1024;
+  const int64_t words = (bins + 31) / 32;
+  const int64_t ccap = std::max<int64_t>(1, std::min<int64_t>(maxc, bins));  // >= every nnz
+  const int64_t kcap = std::min<int64_t>(maxc, 4096);
+  if (!weighted && sparse && words * 8 + ccap * 4 + kcap * 4 <= 160 * 1024) {
+    const int cap = static_cast<int>(std::max<int64_t>(kcap, 1));
+    const size_t smem = size_t(words) * 8 + size_t(ccap) * 4 + size_t(cap) * 4;
+    auto k = cells_bitmap_kernel<D, 256>;
+    VDFCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    int occ = 0;
+    VDFCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, smem));
+    const int grid = std::max(1, std::min(c.n_cells, ctx->sm_count * std::max(occ, 1)));
+    VelPtrs vp{{c.vel[0], c.vel[1], c.vel[2]}};
+    VDFCG_LAUNCH(ctx, "cells_bitmap",
+                 k<<<grid, 256, smem, ctx->stream>>>(vp, c.offsets, c.n_cells, g, static_cast<int>(words),
+                                                     static_cast<int>(ccap), cap, out.nnz, out.keys, out.counts, out.oor,
+                                                     out.in_range));
+    done = true;
+  }
+  if (!done && maxc <= 8192 && (weighted || sparse)) {
     done = weighted ? try_sort_path<D, true>(ctx, c, out, g, binbits, maxc, err)
                     : try_sort_path<D, false>(ctx, c, out, g, binbits, maxc, err);
   }
