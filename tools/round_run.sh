@@ -11,7 +11,6 @@ timeout 600 python bench.py --impl reference > $OUT/bench_ref.json 2> $OUT/bench
 CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu"
 timeout 600 $CMD > $OUT/plain.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1
-PCMD="python tools/prof_cells.py --cells 16384 --reps 1"
-timeout 300 $PCMD > $OUT/plain2.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"em_kernel|cells_sort" -c 2 -o $OUT/prof_round $PCMD > $OUT/ncu_full.log 2>&1
+# full capture of the two top kernels on the SAME bench command (first launch of each)
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"em_kernel|cells_bitmap|cells_sort|cells_dense" -c 2 -o $OUT/prof_round $CMD > $OUT/ncu_full.log 2>&1
 echo done
