@@ -92,42 +92,70 @@ VDFCG_DEV void em_pass(const Src& src, int n, EmState<D, K>& S, double* red) {
   for (int i = 0; i < K; ++i)
 #pragma unroll
     for (int j = 0; j < NS; ++j) acc[i][j] = 0.0;
-  Kahan ll;
-  for (int p = threadIdx.x; p < n; p += blockDim.x) {
-    double z[D], w;
-    src.load(p, z, w);
+  // Per-lane plain sum (<= a few hundred terms) + the fixed-order tree below: the
+  // reference's Kahan sum (gaussian.hpp:55-68) guards a single sequential sum over all
+  // points; here the error stays ~1e-15 relative either way.
+  double ll = 0.0;
+  // NP points per lane per iteration (p, p + blockDim, ...): every shared-memory parameter
+  // load serves all of them and their dependency chains interleave. The per-lane accumulation
+  // order (p, p + B, p + 2B, ...) is unchanged, so results are bitwise the same as one
+  // point at a time. A missing second point gets weight 0 and skips the log-likelihood.
+  constexpr int NP = 1;  // 2 measured slower: the extra registers cost more occupancy
+  for (int p0 = threadIdx.x; p0 < n; p0 += NP * blockDim.x) {
+    double z[NP][D], w[NP];
+    bool valid[NP];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const int p = p0 + q * blockDim.x;
+      valid[q] = p < n;
+      src.load(valid[q] ? p : p0, z[q], w[q]);
+      if (!valid[q]) w[q] = 0.0;
+    }
     // Every slot i < K is evaluated: slots >= m carry cst = -inf, A = b = mu = 0, so they
     // add exactly nothing to s and their accumulators are never read (no per-slot branch).
-    double lp[K];
-    double mx = -dinf();
+    double lp[NP][K];
+    double mx[NP];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) mx[q] = -dinf();
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-      lp[i] = comp_logp_affine<D>(z, S.A[i], S.bv[i], S.cst[i]);
-      mx = fmax(mx, lp[i]);
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {
+        lp[q][i] = comp_logp_affine<D>(z[q], S.A[i], S.bv[i], S.cst[i]);
+        mx[q] = lp[q][i] > mx[q] ? lp[q][i] : mx[q];
+      }
     }
-    double s = 0.0;
+    double ws[NP];
 #pragma unroll
-    for (int i = 0; i < K; ++i) {
-      lp[i] = exp_nonpos(lp[i] - mx, S.exp2tab);
-      s += lp[i];
+    for (int q = 0; q < NP; ++q) {
+      double sum = 0.0;
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        lp[q][i] = exp_nonpos(lp[q][i] - mx[q], S.exp2tab);
+        sum += lp[q][i];
+      }
+      if (!EXACT && valid[q]) ll += w[q] * (mx[q] + log(sum));
+      ws[q] = w[q] * rcp_newton(sum);
     }
-    if (!EXACT) ll.add(w * (mx + log(s)));
-    const double ws = w * rcp_newton(s);
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-      {
-        if (EXACT && !((S.exact_mask >> i) & 1)) continue;
-        const double g = lp[i] * ws;
+      if (EXACT && !((S.exact_mask >> i) & 1)) continue;
+      double c[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) c[a] = EXACT ? S.mu_new[i][a] : S.mu[i][a];
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {
+        const double g = lp[q][i] * ws[q];
         double dl[D];
 #pragma unroll
-        for (int a = 0; a < D; ++a) dl[a] = z[a] - (EXACT ? S.mu_new[i][a] : S.mu[i][a]);
+        for (int a = 0; a < D; ++a) dl[a] = z[q][a] - c[a];
         acc[i][0] += g;
 #pragma unroll
         for (int a = 0; a < D; ++a) {
           const double gd = g * dl[a];
           acc[i][1 + a] += gd;
 #pragma unroll
-          for (int b = a; b < D; ++b) acc[i][1 + D + uidx<D>(a, b)] += gd * dl[b];
+          for (int b2 = a; b2 < D; ++b2) acc[i][1 + D + uidx<D>(a, b2)] += gd * dl[b2];
         }
       }
     }
@@ -146,7 +174,7 @@ VDFCG_DEV void em_pass(const Src& src, int n, EmState<D, K>& S, double* red) {
     }
   }
   if (!EXACT) {
-    const double v = warp_sum(ll.value());
+    const double v = warp_sum(ll);
     if (lane == 0) red[warp * W + K * NS] = v;
   }
   __syncthreads();
@@ -561,7 +589,7 @@ VDFCG_DEV int key_prologue(const KeyCells& kc, int c, const EmConfig& cfg, EmSta
 }
 
 template <int D, int K, bool KEYS>
-__global__ void __launch_bounds__(256, (K <= 4 ? 2 : 1)) em_kernel(KeyCells kc, CoordArgs ca, EmConfig cfg,
+__global__ void __launch_bounds__(256) __maxnreg__(K <= 4 ? 128 : 255) em_kernel(KeyCells kc, CoordArgs ca, EmConfig cfg,
                                                  EmOut out, int* counter, int red_stride) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   EmState<D, K>& S = *reinterpret_cast<EmState<D, K>*>(smem_raw);
