@@ -35,6 +35,7 @@ struct EmState {
   double st[K][NS];
   double st2[K][NS];
   double exp2tab[64];
+  double logtab[256];
   double ll;
   double prev_ll;
   Frame fr;
@@ -134,7 +135,7 @@ VDFCG_DEV void em_pass(const Src& src, int n, EmState<D, K>& S, double* red) {
         lp[q][i] = exp_nonpos(lp[q][i] - mx[q], S.exp2tab);
         sum += lp[q][i];
       }
-      if (!EXACT && valid[q]) ll += w[q] * (mx[q] + log(sum));
+      if (!EXACT && valid[q]) ll += w[q] * (mx[q] + log_ge1(sum, S.logtab));
       ws[q] = w[q] * rcp_newton(sum);
     }
 #pragma unroll
@@ -598,6 +599,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(K <= 4 ? 128 : 255) em_kernel
   double* ztab = red + (blockDim.x >> 5) * red_stride;
   const int n_cells = KEYS ? kc.n_cells : 1;
   for (int j = threadIdx.x; j < 64; j += blockDim.x) S.exp2tab[j] = kExp2Tab[j];
+  for (int j = threadIdx.x; j < 256; j += blockDim.x) S.logtab[j] = kLogTab[j];
   for (;;) {
     if (threadIdx.x == 0) S.cell = atomicAdd(counter, 1);
     __syncthreads();
