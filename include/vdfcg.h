@@ -125,6 +125,9 @@ int vdfcg_ctx_kernel_times(vdfcg_ctx* ctx, int32_t max_entries, char* names /* m
                            double* ms, int64_t* launches, int32_t* n_entries);
 /* Total kernel launches issued by this context since creation. */
 int64_t vdfcg_ctx_launch_count(vdfcg_ctx* ctx);
+/* Diagnostics since creation/last reset: number of (fit, iteration) pairs that ran the
+ * exact second M-step pass. reset != 0 zeroes the counters. */
+int vdfcg_ctx_diagnostics(vdfcg_ctx* ctx, int64_t* exact_passes, int reset);
 
 /* ------------------------------------------------------------------------- */
 /* Histogram (histogram.hpp / histogram.cpp)                                  */

@@ -18,7 +18,7 @@ from . import _abi, _marshal
 from .types import (AxisRange, FitConfig, GmmModel, InvalidArgument, ModelMeta,  # noqa: F401
                     ParticleSet, WeightedPoints)
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libvdfcg.so")
+LIB_PATH = os.environ.get("VDFCG_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libvdfcg.so")
 
 _lib = None
 _lib_lock = threading.Lock()
@@ -37,6 +37,7 @@ def _bind(lib) -> None:
         "vdfcg_ctx_reset_timing": (C.c_int, [vp]),
         "vdfcg_ctx_kernel_times": (C.c_int, [vp, i32, vp, vp, vp, vp]),
         "vdfcg_ctx_launch_count": (i64, [vp]),
+        "vdfcg_ctx_diagnostics": (C.c_int, [vp, vp, C.c_int]),
         "vdfcg_bin_particles": (C.c_int, [vp, vp, i64, i32, vp, i32, i32, f64, f64, f64, f64, vp, vp]),
         "vdfcg_all_planes": (C.c_int, [vp, vp, i64, i32, vp, i32, f64, f64, vp, vp]),
         "vdfcg_to_weighted_points": (C.c_int, [vp, vp, i32, f64, f64, f64, f64, i32, i64, vp, vp, vp, vp]),
@@ -134,6 +135,13 @@ class Context:
 
     def launch_count(self) -> int:
         return int(lib().vdfcg_ctx_launch_count(self.handle))
+
+    def exact_passes(self, reset: bool = False) -> int:
+        """(fit, iteration) pairs that ran the exact second M-step pass."""
+        v = C.c_int64(0)
+        _marshal.check(lib().vdfcg_ctx_diagnostics(self.handle, C.byref(v), 1 if reset else 0),
+                       last_error)
+        return int(v.value)
 
 
 _tls = threading.local()

@@ -150,6 +150,8 @@ int vdfcg_ctx_create(int device, vdfcg_ctx** out) {
     VDFCG_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
     c->stream = c->own_stream;
     VDFCG_CUDA(cudaHostAlloc(&c->pinned, 4096, cudaHostAllocDefault));
+    VDFCG_CUDA(cudaMalloc(&c->diag, 8 * sizeof(unsigned long long)));
+    VDFCG_CUDA(cudaMemset(c->diag, 0, 8 * sizeof(unsigned long long)));
     *out = c;
   });
 }
@@ -166,6 +168,7 @@ int vdfcg_ctx_destroy(vdfcg_ctx* ctx) {
     }
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->diag) cudaFree(ctx->diag);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
   });
@@ -221,5 +224,17 @@ int vdfcg_ctx_kernel_times(vdfcg_ctx* ctx, int32_t max_entries, char* names, dou
 }
 
 int64_t vdfcg_ctx_launch_count(vdfcg_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int vdfcg_ctx_diagnostics(vdfcg_ctx* ctx, int64_t* exact_passes, int reset) {
+  return guard_impl([&] {
+    if (!ctx) throw InvalidArgument("null context");
+    VDFCG_CUDA(cudaSetDevice(ctx->device));
+    unsigned long long h[8];
+    VDFCG_CUDA(cudaMemcpyAsync(h, ctx->diag, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    if (exact_passes) *exact_passes = static_cast<int64_t>(h[0]);
+    if (reset) VDFCG_CUDA(cudaMemsetAsync(ctx->diag, 0, sizeof(h), ctx->stream));
+  });
+}
 
 }  // extern "C"

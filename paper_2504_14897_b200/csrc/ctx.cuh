@@ -52,6 +52,8 @@ struct vdfcg_ctx {
   std::vector<Chunk> chunks;
   // pinned scalar readback slot
   void* pinned = nullptr;
+  // device diagnostics counters: [0] exact second EM passes run
+  unsigned long long* diag = nullptr;
   // timing
   bool timing = false;
   struct Pending {

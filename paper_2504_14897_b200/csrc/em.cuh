@@ -41,6 +41,7 @@ struct EmConfig {
   const double* warm_mu;
   const double* warm_cov;
   const double* uniforms;   // [16*3] mt19937_64(seed) uniforms (device)
+  unsigned long long* exact_counter;  // optional diagnostics: exact second passes run
 };
 
 struct EmOut {

@@ -19,17 +19,31 @@ struct NStat {
   static constexpr int value = 1 + D + D * (D + 1) / 2;
 };
 
+// Lanes per point in the point pass (component split, see em_pass). 2 for K in 2..4:
+// each lane of a pair owns K/2 components' accumulators, halving the registers.
+#ifndef VDFCG_SPLIT
+#define VDFCG_SPLIT 1
+#endif
+template <int K>
+struct Split {
+  static constexpr int SP = (K >= 2 && K <= 4) ? VDFCG_SPLIT : 1;
+  static constexpr int KL = (K + SP - 1) / SP;  // component slots per lane
+  static constexpr int KPAD = KL * SP;          // padded slot count
+};
+
 template <int D, int K>
 struct EmState {
   static constexpr int NS = NStat<D>::value;
+  static constexpr int KP = Split<K>::KPAD;
   double alpha[K];
   double mu[K][D];
   double cov[K][9];
   double Lo[K][3];  // L(1,0), L(2,0), L(2,1)
   double rd[K][3];  // 1 / L(a,a)
-  double cst[K];    // -0.5 (d log 2pi + log det) + log alpha ; -inf when dead
-  double A[K][6];   // L^-1 packed (affine form used by the point pass)
-  double bv[K][3];  // L^-1 mu
+  double cst[KP];   // -0.5 (d log 2pi + log det) + log alpha ; -inf when dead or padding
+  double A[KP][6];  // L^-1 packed (affine form used by the point pass)
+  double bv[KP][3]; // L^-1 mu
+  double muc[KP][3];  // centre of the moment sums (mu_old, or mu_new in the exact pass)
   double mu_new[K][D];
   double sig1[K][9];
   double st[K][NS];
@@ -87,91 +101,105 @@ VDFCG_DEV constexpr int uidx(int a, int b) {  // packed upper index, a <= b
 template <int D, int K, bool EXACT, class Src>
 VDFCG_DEV void em_pass(const Src& src, int n, EmState<D, K>& S, double* red) {
   constexpr int NS = NStat<D>::value;
+  constexpr int SP = Split<K>::SP, KL = Split<K>::KL;
   const int m = S.m;
-  double acc[K][NS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, G = blockDim.x >> 5;
+  const int part = lane % SP;       // this lane owns slots [part*KL, part*KL + KL)
+  const int slot0 = part * KL;
+  constexpr int GPW = 32 / SP;      // points per warp per iteration
+  double acc[KL][NS];
 #pragma unroll
-  for (int i = 0; i < K; ++i)
+  for (int j = 0; j < KL; ++j)
 #pragma unroll
-    for (int j = 0; j < NS; ++j) acc[i][j] = 0.0;
-  // Per-lane plain sum (<= a few hundred terms) + the fixed-order tree below: the
-  // reference's Kahan sum (gaussian.hpp:55-68) guards a single sequential sum over all
-  // points; here the error stays ~1e-15 relative either way.
+    for (int t = 0; t < NS; ++t) acc[j][t] = 0.0;
+  // Per-lane plain sum + the fixed-order tree below: the reference's Kahan sum
+  // (gaussian.hpp:55-68) guards one sequential sum over all points; the error here stays
+  // ~1e-15 relative either way.
   double ll = 0.0;
-  // NP points per lane per iteration (p, p + blockDim, ...): every shared-memory parameter
-  // load serves all of them and their dependency chains interleave. The per-lane accumulation
-  // order (p, p + B, p + 2B, ...) is unchanged, so results are bitwise the same as one
-  // point at a time. A missing second point gets weight 0 and skips the log-likelihood.
-  constexpr int NP = 1;  // 2 measured slower: the extra registers cost more occupancy
-  for (int p0 = threadIdx.x; p0 < n; p0 += NP * blockDim.x) {
-    double z[NP][D], w[NP];
-    bool valid[NP];
+  // Each point is owned by SP adjacent lanes, each evaluating its own KL component slots;
+  // the max and the sum of the log-sum-exp are combined with SP-lane xor shuffles. The
+  // loop is warp-uniform (a missing point gets weight 0 and adds nothing). Slots >= m
+  // carry cst = -inf, A = b = 0, so they add exactly nothing and are never read.
+  for (int b0 = warp * GPW; b0 < n; b0 += G * GPW) {
+    const int p = b0 + lane / SP;
+    const bool valid = p < n;
+    double z[D], w;
+    src.load(valid ? p : b0, z, w);
+    if (!valid) w = 0.0;
+    double lp[KL];
+    double mx = -dinf();
 #pragma unroll
-    for (int q = 0; q < NP; ++q) {
-      const int p = p0 + q * blockDim.x;
-      valid[q] = p < n;
-      src.load(valid[q] ? p : p0, z[q], w[q]);
-      if (!valid[q]) w[q] = 0.0;
+    for (int j = 0; j < KL; ++j) {
+      const int i = slot0 + j;
+      lp[j] = comp_logp_affine<D>(z, S.A[i], S.bv[i], S.cst[i]);
+      mx = lp[j] > mx ? lp[j] : mx;
     }
-    // Every slot i < K is evaluated: slots >= m carry cst = -inf, A = b = mu = 0, so they
-    // add exactly nothing to s and their accumulators are never read (no per-slot branch).
-    double lp[NP][K];
-    double mx[NP];
 #pragma unroll
-    for (int q = 0; q < NP; ++q) mx[q] = -dinf();
+    for (int o = 1; o < SP; o <<= 1) {
+      const double other = __shfl_xor_sync(0xffffffffu, mx, o);
+      mx = other > mx ? other : mx;
+    }
+    double sum = 0.0;
 #pragma unroll
-    for (int i = 0; i < K; ++i) {
+    for (int j = 0; j < KL; ++j) {
+      lp[j] = exp_nonpos(lp[j] - mx, S.exp2tab);
+      sum += lp[j];
+    }
 #pragma unroll
-      for (int q = 0; q < NP; ++q) {
-        lp[q][i] = comp_logp_affine<D>(z[q], S.A[i], S.bv[i], S.cst[i]);
-        mx[q] = lp[q][i] > mx[q] ? lp[q][i] : mx[q];
+    for (int o = 1; o < SP; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (!EXACT && part == 0) ll += w * (mx + log_ge1(sum, S.logtab));
+    const double ws = w * rcp_newton(sum);
+    if (!EXACT) {
+      // Pass 1 accumulates about the frame origin (z is the normalised coordinate,
+      // |z| <= 1): the D(D+1)/2 products are shared by every component. The M-step
+      // turns the raw sums into Eq. 9 (Sigma = S/m - mu mu^T with mu = t/m, the
+      // reference's own mean) and runs the exact pass where the cancellation could cost
+      // more than ~1e-12 of the smallest eigenvalue.
+      double zz[D * (D + 1) / 2];
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int b2 = a; b2 < D; ++b2) zz[uidx<D>(a, b2)] = z[a] * z[b2];
+#pragma unroll
+      for (int j = 0; j < KL; ++j) {
+        const double g = lp[j] * ws;
+        acc[j][0] += g;
+#pragma unroll
+        for (int a = 0; a < D; ++a) acc[j][1 + a] = fma(g, z[a], acc[j][1 + a]);
+#pragma unroll
+        for (int u = 0; u < D * (D + 1) / 2; ++u) acc[j][1 + D + u] = fma(g, zz[u], acc[j][1 + D + u]);
       }
-    }
-    double ws[NP];
+    } else {
 #pragma unroll
-    for (int q = 0; q < NP; ++q) {
-      double sum = 0.0;
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        lp[q][i] = exp_nonpos(lp[q][i] - mx[q], S.exp2tab);
-        sum += lp[q][i];
-      }
-      if (!EXACT && valid[q]) ll += w[q] * (mx[q] + log_ge1(sum, S.logtab));
-      ws[q] = w[q] * rcp_newton(sum);
-    }
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-      if (EXACT && !((S.exact_mask >> i) & 1)) continue;
-      double c[D];
-#pragma unroll
-      for (int a = 0; a < D; ++a) c[a] = EXACT ? S.mu_new[i][a] : S.mu[i][a];
-#pragma unroll
-      for (int q = 0; q < NP; ++q) {
-        const double g = lp[q][i] * ws[q];
+      for (int j = 0; j < KL; ++j) {
+        const int i = slot0 + j;
+        if (!((S.exact_mask >> i) & 1)) continue;
+        const double g = lp[j] * ws;
         double dl[D];
 #pragma unroll
-        for (int a = 0; a < D; ++a) dl[a] = z[q][a] - c[a];
-        acc[i][0] += g;
+        for (int a = 0; a < D; ++a) dl[a] = z[a] - S.muc[i][a];
+        acc[j][0] += g;
 #pragma unroll
         for (int a = 0; a < D; ++a) {
           const double gd = g * dl[a];
-          acc[i][1 + a] += gd;
+          acc[j][1 + a] += gd;
 #pragma unroll
-          for (int b2 = a; b2 < D; ++b2) acc[i][1 + D + uidx<D>(a, b2)] += gd * dl[b2];
+          for (int b2 = a; b2 < D; ++b2) acc[j][1 + D + uidx<D>(a, b2)] += gd * dl[b2];
         }
       }
     }
   }
-  // fixed-order reduction: lanes (xor tree) -> warps (ascending)
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, G = blockDim.x >> 5;
+  // fixed-order reduction: lanes of the same part (xor tree) -> warps (ascending)
   constexpr int W = K * NS + 1;
 #pragma unroll
-  for (int i = 0; i < K; ++i) {
-    if (i < m) {
+  for (int j = 0; j < KL; ++j) {
 #pragma unroll
-      for (int j = 0; j < NS; ++j) {
-        const double v = warp_sum(acc[i][j]);
-        if (lane == 0) red[warp * W + i * NS + j] = v;
-      }
+    for (int t = 0; t < NS; ++t) {
+      double v = acc[j][t];
+#pragma unroll
+      for (int o = 16; o >= SP; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      const int i = slot0 + j;
+      if (lane < SP && i < m) red[warp * W + i * NS + t] = v;
     }
   }
   if (!EXACT) {
@@ -225,14 +253,17 @@ VDFCG_DEV void run_fit(const Src& src, int n, EmState<D, K>& S, double* red, con
       if (lane < S.m) {
         dead = !prep_component<D>(S.cov[lane], S.alpha[lane], S.Lo[lane], S.rd[lane], &S.cst[lane]);
         affine_from_chol<D>(S.mu[lane], S.Lo[lane], S.rd[lane], S.A[lane], S.bv[lane]);
-      } else if (lane < K) {  // inactive slot: contributes exactly zero
+#pragma unroll
+        for (int a = 0; a < D; ++a) S.muc[lane][a] = S.mu[lane][a];
+      } else if (lane < EmState<D, K>::KP) {  // inactive / padding slot: contributes zero
         S.cst[lane] = -dinf();
 #pragma unroll
         for (int e = 0; e < 6; ++e) S.A[lane][e] = 0.0;
 #pragma unroll
-        for (int a = 0; a < 3; ++a) S.bv[lane][a] = 0.0;
-#pragma unroll
-        for (int a = 0; a < D; ++a) S.mu[lane][a] = 0.0;
+        for (int a = 0; a < 3; ++a) {
+          S.bv[lane][a] = 0.0;
+          S.muc[lane][a] = 0.0;
+        }
       }
       const unsigned dm = __ballot_sync(0xffffffffu, dead);
       if (lane == 0) {
@@ -259,13 +290,13 @@ VDFCG_DEV void run_fit(const Src& src, int n, EmState<D, K>& S, double* red, con
         const bool starved = !(mass > S.fr.total * kMassFloorRel);
         if (!bad && !starved) {
           const double inv = 1.0 / mass;
-          double db[D];
-          double dd = 0.0;
+          double mn[D];
+          double dd = 0.0;  // squared distance of the new mean from the accumulation origin
 #pragma unroll
           for (int a = 0; a < D; ++a) {
-            db[a] = S.st[i][1 + a] * inv;
-            S.mu_new[i][a] = S.mu[i][a] + db[a];
-            dd += db[a] * db[a];
+            mn[a] = S.st[i][1 + a] * inv;
+            S.mu_new[i][a] = mn[a];
+            dd += mn[a] * mn[a];
           }
           Sym3 s1;
 #pragma unroll
@@ -274,15 +305,15 @@ VDFCG_DEV void run_fit(const Src& src, int n, EmState<D, K>& S, double* red, con
           for (int a = 0; a < D; ++a)
 #pragma unroll
             for (int b = a; b < D; ++b)
-              s1(a, b) = S.st[i][1 + D + uidx<D>(a, b)] * inv - db[a] * db[b];
+              s1(a, b) = S.st[i][1 + D + uidx<D>(a, b)] * inv - mn[a] * mn[b];
           symmetrize_from_upper<D>(s1);
 #pragma unroll
           for (int e = 0; e < 9; ++e) S.sig1[i][e] = s1.a[e];
-          // The shifted form loses ~eps*|d|^2 absolute; recompute Eq. 9 around the new
-          // mean whenever that could reach 1e-12 of the smallest eigenvalue (or the LLT
-          // fails), so the collapse test sees reference-grade numerics. lmin >= lb.
+          // Raw moments lose ~eps*|mu|^2 absolute; recompute Eq. 9 around the new mean
+          // whenever that could exceed ~1e-12 of the smallest eigenvalue (lmin >= lb) or
+          // the LLT fails, so the collapse test and the parameters see reference numerics.
           const double lb = lmin_lower_bound<D>(s1);
-          need = !(lb > 0.0) || dd > 1e3 * lb;
+          need = !(lb > 0.0) || dd > 1e4 * lb;
           cert = lb > 1e-14 * trace3<D>(s1);
         }
       }
@@ -300,7 +331,15 @@ VDFCG_DEV void run_fit(const Src& src, int n, EmState<D, K>& S, double* red, con
     }
     __syncthreads();
     if (S.status) break;
-    if (S.exact_mask) em_pass<D, K, true>(src, n, S, red);
+    if (S.exact_mask) {
+      if (threadIdx.x == 0 && cfg.exact_counter) atomicAdd(cfg.exact_counter, 1ull);
+      if (warp == 0 && lane < S.m && ((S.exact_mask >> lane) & 1)) {
+#pragma unroll
+        for (int a = 0; a < D; ++a) S.muc[lane][a] = S.mu_new[lane][a];
+      }
+      __syncthreads();
+      em_pass<D, K, true>(src, n, S, red);
+    }
 
     // ---- M-step part 2: covariances, collapse test, repair (wgmm.cpp:299-316)
     if (warp == 0) {

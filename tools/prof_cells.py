@@ -37,6 +37,7 @@ for _ in range(a.reps):
     G.compress_cells(b, cfg, meta, bins=bins, results=res)
 torch.cuda.synchronize()
 print({k: round(v[0] / a.reps, 3) for k, v in ctx.kernel_times().items()})
+print("exact passes per fit-iteration:", ctx.exact_passes() / (a.reps * a.cells * 100.0))
 it = res.iterations.cpu().numpy()
 print("iterations mean", it.mean(), "converged", res.converged.cpu().numpy().mean(),
       "nnz mean", bins.nnz.cpu().numpy().mean())
