@@ -563,23 +563,25 @@ __global__ void __launch_bounds__(BLOCK) cells_bitmap_kernel(
     int cap, int32_t* nnz, uint32_t* __restrict__ keys_out, double* __restrict__ counts_out,
     double* oor_out, double* in_range) {
   using Scan = cub::BlockScan<unsigned, BLOCK>;
-  using Reduce = cub::BlockReduce<unsigned, BLOCK>;
   __shared__ typename Scan::TempStorage ss;
-  __shared__ typename Reduce::TempStorage rs;
+  __shared__ unsigned s_oor, s_nnz;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned* bitmap = reinterpret_cast<unsigned*>(smem_raw);  // [words]
   unsigned* wpre = bitmap + words;                           // [words] exclusive prefix
   unsigned* cnt = wpre + words;                              // [ccap >= max nnz] per-rank counts
   unsigned* kbuf = cnt + ccap;                               // [cap] keys of this cell
   const int wpt = (words + BLOCK - 1) / BLOCK;
+  // bitmap and counters start zero and are re-zeroed by the emit phase of every cell
+  for (int t = threadIdx.x; t < words; t += BLOCK) bitmap[t] = 0u;
+  for (int t = threadIdx.x; t < ccap; t += BLOCK) cnt[t] = 0u;
+  if (threadIdx.x == 0) s_oor = 0u;
+  __syncthreads();
   for (int c = blockIdx.x; c < n_cells; c += gridDim.x) {
     const int64_t b = offsets[c];
     const int nc = static_cast<int>(offsets[c + 1] - b);
-    for (int t = threadIdx.x; t < words; t += BLOCK) bitmap[t] = 0u;
-    for (int t = threadIdx.x; t < min(nc, ccap); t += BLOCK) cnt[t] = 0u;
-    __syncthreads();
+    // 1. occupancy bits (8 particles = 24 independent loads in flight per thread)
     unsigned oor = 0;
-    constexpr int U = 8;  // 8 particles (24 independent 8-byte loads) in flight per thread
+    constexpr int U = 8;
     for (int l0 = threadIdx.x; l0 < nc; l0 += U * BLOCK) {
       int64_t key[U];
 #pragma unroll
@@ -596,7 +598,10 @@ __global__ void __launch_bounds__(BLOCK) cells_bitmap_kernel(
         if (li < cap) kbuf[li] = key[u] < 0 ? 0xffffffffu : static_cast<unsigned>(key[u]);
       }
     }
+    oor = warp_sum(oor);
+    if ((threadIdx.x & 31) == 0 && oor) atomicAdd(&s_oor, oor);
     __syncthreads();
+    // 2. rank of every occupied bin = exclusive prefix of per-word popcounts
     unsigned local = 0;
     for (int k = 0; k < wpt; ++k) {
       const int wi = threadIdx.x * wpt + k;
@@ -612,6 +617,8 @@ __global__ void __launch_bounds__(BLOCK) cells_bitmap_kernel(
       }
     }
     __syncthreads();
+    // 3. count per rank; each particle writes its bin key at its rank (duplicates write
+    //    the same value), so keys come out in ascending order without an emit loop
     for (int li = threadIdx.x; li < nc; li += BLOCK) {
       unsigned key;
       if (li < cap) {
@@ -624,27 +631,22 @@ __global__ void __launch_bounds__(BLOCK) cells_bitmap_kernel(
         const unsigned wd = key >> 5, bit = key & 31;
         const unsigned r = wpre[wd] + __popc(bitmap[wd] & ((1u << bit) - 1u));
         atomicAdd(cnt + r, 1u);
+        keys_out[b + r] = key;
       }
     }
     __syncthreads();
-    for (int k = 0; k < wpt; ++k) {
-      const int wi = threadIdx.x * wpt + k;
-      if (wi >= words) break;
-      unsigned bits = bitmap[wi];
-      unsigned r = wpre[wi];
-      while (bits) {
-        const unsigned bit = __ffs(bits) - 1;
-        keys_out[b + r] = (static_cast<unsigned>(wi) << 5) | bit;
-        counts_out[b + r] = static_cast<double>(cnt[r]);
-        ++r;
-        bits &= bits - 1;
-      }
+    // 4. coalesced emit of the counts; re-zero counters and bitmap for the next cell
+    for (unsigned r = threadIdx.x; r < total; r += BLOCK) {
+      counts_out[b + r] = static_cast<double>(cnt[r]);
+      cnt[r] = 0u;
     }
-    const unsigned to = Reduce(rs).Sum(oor);
+    for (int t = threadIdx.x; t < words; t += BLOCK) bitmap[t] = 0u;
     if (threadIdx.x == 0) {
+      const unsigned to = s_oor;
       nnz[c] = static_cast<int32_t>(total);
       oor_out[c] = static_cast<double>(to);
       in_range[c] = static_cast<double>(nc - static_cast<int>(to));
+      s_oor = 0u;
     }
     __syncthreads();
   }
