@@ -48,7 +48,7 @@ struct EmState {
   double sig1[K][9];
   double st[K][NS];
   double st2[K][NS];
-  double exp2tab[64];
+  double exp2tab[kExpTab];
   double logtab[256];
   double ll;
   double prev_ll;
@@ -637,7 +637,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(K <= 4 ? 128 : 255) em_kernel
   double* red = reinterpret_cast<double*>(smem_raw + st_bytes);
   double* ztab = red + (blockDim.x >> 5) * red_stride;
   const int n_cells = KEYS ? kc.n_cells : 1;
-  for (int j = threadIdx.x; j < 64; j += blockDim.x) S.exp2tab[j] = kExp2Tab[j];
+  for (int j = threadIdx.x; j < kExpTab; j += blockDim.x) S.exp2tab[j] = kExp2Tab[j];
   for (int j = threadIdx.x; j < 256; j += blockDim.x) S.logtab[j] = kLogTab[j];
   for (;;) {
     if (threadIdx.x == 0) S.cell = atomicAdd(counter, 1);
