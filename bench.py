@@ -124,6 +124,17 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def ncu_traffic(config_name):
+    """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of each kernel
+    from the committed `ncu --set full` capture of this bench command (profiles/)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", f"ncu_traffic_{config_name}.json")) as f:
+            d = json.load(f)
+        return {k: v["dram_bytes_per_launch"] for k, v in d["kernels"].items()}
+    except Exception:
+        return {}
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -411,12 +422,13 @@ def run_gpu(args, cfg):
     hbm_peak, hbm_src = peaks()
     steps = args.steps
     em_flops_launch = flops / max(len(batches), 1)  # per launch (one EM launch per species)
+    traffic = ncu_traffic(args.config)
     roofline = None
     if em_n:
         ach = (flops * steps) / (em_ms * 1e-3) / 1e12
         roofline = {"kernel": "em_fit", "bound": "fp64", "achieved": ach, "peak": fp64_peak,
                     "unit": "TFLOP/s", "frac": ach / fp64_peak if fp64_peak else None,
-                    "traffic": None, "peak_source": "measured FP64 FMA probe on this GPU (vdfcg_probe_peaks)",
+                    "traffic": traffic.get("em_fit"), "peak_source": "measured FP64 FMA probe on this GPU (vdfcg_probe_peaks)",
                     "flops_per_launch": em_flops_launch, "avg_launch_ms": em_ms / em_n,
                     "share_of_step": em_ms / max(ms_total if world == 1 else ms_total, 1e-9),
                     "algorithm": f"F(d)={F_D[d]} flops per (point, component, iteration); "
@@ -425,7 +437,8 @@ def run_gpu(args, cfg):
     if h_n:
         ach = (hist_bytes * steps) / (h_ms * 1e-3) / 1e9
         roofline_hist = {"kernel": hist_name, "bound": "hbm", "achieved": ach, "peak": hbm_peak,
-                         "unit": "GB/s", "frac": ach / hbm_peak, "traffic": None,
+                         "unit": "GB/s", "frac": ach / hbm_peak,
+                         "traffic": traffic.get(hist_name.replace("cells_", "cells_")) if hist_name else None,
                          "peak_source": hbm_src, "bytes_per_launch": hist_bytes / len(batches),
                          "avg_launch_ms": h_ms / h_n,
                          "algorithm": "24 B/particle read (u,v,w f64) + 12 B per non-empty bin "
