@@ -263,6 +263,13 @@ int vdfcg_bin_cells(vdfcg_ctx* ctx, const vdfcg_cells* cells, vdfcg_cell_bins* o
 int vdfcg_fit_cells(vdfcg_ctx* ctx, const vdfcg_cells* cells, const vdfcg_cell_bins* bins,
                     const vdfcg_fit_config* cfg, vdfcg_cell_results* out);
 
+/* Time-series warm start (pipeline.cpp:482-564, wgmm.cpp:142-161 per cell): cell c starts
+ * from `warm`'s model of cell c (the previous cycle's results, canonical data space) when
+ * warm->status[c] == 0 and warm->components[c] > 0, else from the seeded random init. */
+int vdfcg_fit_cells_warm(vdfcg_ctx* ctx, const vdfcg_cells* cells, const vdfcg_cell_bins* bins,
+                         const vdfcg_fit_config* cfg, const vdfcg_cell_results* warm,
+                         vdfcg_cell_results* out);
+
 /* Pack every cell's fitted model as a .gmmc record (FORMATS.md). records: capacity
  * bytes; record_offsets: [n_cells+1]. Cells with status != 0 get an empty record. */
 int vdfcg_pack_cells(vdfcg_ctx* ctx, int32_t n_cells, int32_t dimension,
@@ -275,6 +282,13 @@ int vdfcg_compress_cells(vdfcg_ctx* ctx, const vdfcg_cells* cells, const vdfcg_f
                          vdfcg_cell_bins* bins, vdfcg_cell_results* out,
                          const vdfcg_model_meta* meta, uint8_t* records, int64_t capacity,
                          int64_t* record_offsets);
+
+/* compress_cells with the per-cell warm start of vdfcg_fit_cells_warm. */
+int vdfcg_compress_cells_warm(vdfcg_ctx* ctx, const vdfcg_cells* cells,
+                              const vdfcg_fit_config* cfg, const vdfcg_cell_results* warm,
+                              vdfcg_cell_bins* bins, vdfcg_cell_results* out,
+                              const vdfcg_model_meta* meta, uint8_t* records, int64_t capacity,
+                              int64_t* record_offsets);
 
 /* Synthetic cell data for tests/bench (counter-based, deterministic per (seed, species,
  * global particle index)): each cell draws from a 2-component mixture whose drift and

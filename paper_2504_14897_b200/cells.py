@@ -175,18 +175,23 @@ def bin_cells(batch: CellBatch, out: Optional[CellBins] = None) -> CellBins:
 
 
 def fit_cells(batch: CellBatch, bins: CellBins, config: FitConfig, trace: bool = False,
-              out: Optional[CellResults] = None) -> CellResults:
+              out: Optional[CellResults] = None,
+              warm: Optional[CellResults] = None) -> CellResults:
+    """Fit every cell (same FitConfig, pipeline.cpp:144). `warm`: the previous cycle's
+    results — each cell restarts from its own model (time series, pipeline.cpp:482-564)."""
     api = _api()
     d = batch.d
-    warm = _abi.ModelBuffers.from_model(config.warm_start) if config.warm_start is not None else None
-    cfg = _abi.fit_config_struct(config, d, warm)
-    k = max(config.initial_components, warm.k if warm else 0)
+    wm = _abi.ModelBuffers.from_model(config.warm_start) if config.warm_start is not None else None
+    cfg = _abi.fit_config_struct(config, d, wm)
+    k = max(config.initial_components, wm.k if wm else 0, warm.k if warm is not None else 0)
     out = out or CellResults(batch.axes[0], batch.n_cells, d, k,
                              config.max_em_iterations if trace else 0)
     bs = bins.struct()
     rs = out.struct()
-    _check(api.lib().vdfcg_fit_cells(api.context().handle, C.byref(batch.struct), C.byref(bs),
-                                     C.byref(cfg), C.byref(rs)))
+    ws = warm.struct() if warm is not None else None
+    _check(api.lib().vdfcg_fit_cells_warm(api.context().handle, C.byref(batch.struct), C.byref(bs),
+                                          C.byref(cfg), C.byref(ws) if ws is not None else None,
+                                          C.byref(rs)))
     return out
 
 
@@ -208,13 +213,15 @@ def pack_cells(results: CellResults, meta: ModelMeta):
 
 def compress_cells(batch: CellBatch, config: FitConfig, meta: Optional[ModelMeta] = None,
                    trace: bool = False, bins: Optional[CellBins] = None,
-                   results: Optional[CellResults] = None, keep_bins: bool = True):
-    """bin -> fit (-> pack) in one device pass. Returns (bins, results, records, offsets)."""
+                   results: Optional[CellResults] = None, keep_bins: bool = True,
+                   warm: Optional[CellResults] = None):
+    """bin -> fit (-> pack) in one device pass. Returns (bins, results, records, offsets).
+    `warm`: per-cell warm start from the previous cycle's results (see fit_cells)."""
     api = _api()
     d = batch.d
-    warm = _abi.ModelBuffers.from_model(config.warm_start) if config.warm_start is not None else None
-    cfg = _abi.fit_config_struct(config, d, warm)
-    k = max(config.initial_components, warm.k if warm else 0)
+    wm = _abi.ModelBuffers.from_model(config.warm_start) if config.warm_start is not None else None
+    cfg = _abi.fit_config_struct(config, d, wm)
+    k = max(config.initial_components, wm.k if wm else 0, warm.k if warm is not None else 0)
     like = batch.axes[0]
     if keep_bins and bins is None:
         bins = CellBins.alloc(batch)
@@ -230,10 +237,11 @@ def compress_cells(batch: CellBatch, config: FitConfig, meta: Optional[ModelMeta
         cap = batch.n_cells * per
         rec = _empty(like, (max(cap, 1),), "u8")
         offs = _empty(like, (batch.n_cells + 1,), "i64")
-    _check(api.lib().vdfcg_compress_cells(api.context().handle, C.byref(batch.struct), C.byref(cfg),
-                                          C.byref(bs) if bins is not None else None, C.byref(rs),
-                                          C.byref(ms) if ms is not None else None, _ptr(rec), cap,
-                                          _ptr(offs)))
+    ws = warm.struct() if warm is not None else None
+    _check(api.lib().vdfcg_compress_cells_warm(
+        api.context().handle, C.byref(batch.struct), C.byref(cfg),
+        C.byref(ws) if ws is not None else None, C.byref(bs) if bins is not None else None,
+        C.byref(rs), C.byref(ms) if ms is not None else None, _ptr(rec), cap, _ptr(offs)))
     if rec is not None:
         rec = rec[:int(offs[-1])]
     return bins, results, rec, offs

@@ -732,12 +732,30 @@ static EmOut results_dev(vdfcg_ctx* ctx, int n_cells, int d, vdfcg_cell_results*
 static bool any_host(const std::vector<std::function<void()>>& fin) { return !fin.empty(); }
 
 static void fit_cells_dev(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& b,
-                          const vdfcg_fit_config* cfg, const EmOut& o) {
-  if (o.K < std::max(cfg->initial_components, cfg->warm_start ? cfg->warm_start->components : 0))
+                          const vdfcg_fit_config* cfg, const EmOut& o,
+                          const vdfcg_cell_results* warm = nullptr) {
+  const int kw = warm ? warm->capacity_components : 0;
+  if (warm && (kw < 1 || kw > VDFCG_MAX_COMPONENTS))
+    throw InvalidArgument("warm cell results must have capacity_components in 1..16");
+  if (o.K < std::max({cfg->initial_components, cfg->warm_start ? cfg->warm_start->components : 0, kw}))
     throw InvalidArgument("cell results capacity_components too small");
   if (o.trace_cap && o.trace_cap < cfg->max_em_iterations)
     throw InvalidArgument("cell results capacity_trace too small");
   EmConfig e = make_em_config(ctx, cfg, c.d);
+  if (warm) {  // per-cell warm start from a previous (device or host) results buffer
+    const size_t nc = c.n_cells;
+    const int32_t* st = warm->status ? stage_in(ctx, warm->status, nc).dev : nullptr;
+    if (!warm->components || !warm->weights || !warm->means || !warm->covariances)
+      throw InvalidArgument("warm cell results need components, weights, means, covariances");
+    const int32_t* cm = stage_in(ctx, warm->components, nc).dev;
+    int32_t* wm = arena<int32_t>(ctx, nc);
+    launch_warm_m(ctx, c.n_cells, st, cm, wm);
+    e.cell_warm_m = wm;
+    e.cell_warm_K = kw;
+    e.cell_warm_w = stage_in(ctx, warm->weights, nc * kw).dev;
+    e.cell_warm_mu = stage_in(ctx, warm->means, nc * kw * c.d).dev;
+    e.cell_warm_cov = stage_in(ctx, warm->covariances, nc * kw * c.d * c.d).dev;
+  }
   KeyCells kc{};
   kc.n_cells = c.n_cells;
   kc.offsets = c.offsets;
@@ -770,6 +788,12 @@ int vdfcg_bin_cells(vdfcg_ctx* ctx, const vdfcg_cells* cells, vdfcg_cell_bins* o
 
 int vdfcg_fit_cells(vdfcg_ctx* ctx, const vdfcg_cells* cells, const vdfcg_cell_bins* bins,
                     const vdfcg_fit_config* cfg, vdfcg_cell_results* out) {
+  return vdfcg_fit_cells_warm(ctx, cells, bins, cfg, nullptr, out);
+}
+
+int vdfcg_fit_cells_warm(vdfcg_ctx* ctx, const vdfcg_cells* cells, const vdfcg_cell_bins* bins,
+                         const vdfcg_fit_config* cfg, const vdfcg_cell_results* warm,
+                         vdfcg_cell_results* out) {
   return guard_impl([&] {
     begin(ctx);
     if (!cells || !bins) throw InvalidArgument("null argument");
@@ -797,7 +821,7 @@ int vdfcg_fit_cells(vdfcg_ctx* ctx, const vdfcg_cells* cells, const vdfcg_cell_b
     b.in_range = stage_in(ctx, bins->in_range, c.n_cells).dev;
     std::vector<std::function<void()>> fin;
     EmOut o = results_dev(ctx, c.n_cells, c.d, out, fin);
-    fit_cells_dev(ctx, c, b, cfg, o);
+    fit_cells_dev(ctx, c, b, cfg, o, warm);
     for (auto& f : fin) f();
     if (any_host(fin)) sync(ctx);
   });
@@ -841,6 +865,15 @@ int vdfcg_compress_cells(vdfcg_ctx* ctx, const vdfcg_cells* cells, const vdfcg_f
                          vdfcg_cell_bins* bins, vdfcg_cell_results* out,
                          const vdfcg_model_meta* meta, uint8_t* records, int64_t capacity,
                          int64_t* record_offsets) {
+  return vdfcg_compress_cells_warm(ctx, cells, cfg, nullptr, bins, out, meta, records, capacity,
+                                   record_offsets);
+}
+
+int vdfcg_compress_cells_warm(vdfcg_ctx* ctx, const vdfcg_cells* cells,
+                              const vdfcg_fit_config* cfg, const vdfcg_cell_results* warm,
+                              vdfcg_cell_bins* bins, vdfcg_cell_results* out,
+                              const vdfcg_model_meta* meta, uint8_t* records, int64_t capacity,
+                              int64_t* record_offsets) {
   return guard_impl([&] {
     begin(ctx);
     CellsDev c = stage_cells(ctx, cells);
@@ -849,7 +882,7 @@ int vdfcg_compress_cells(vdfcg_ctx* ctx, const vdfcg_cells* cells, const vdfcg_f
     CellBinsDev b = bins_dev(ctx, c, bins, fin);
     EmOut o = results_dev(ctx, c.n_cells, c.d, out, fin);
     launch_bin_cells(ctx, c, b);
-    fit_cells_dev(ctx, c, b, cfg, o);
+    fit_cells_dev(ctx, c, b, cfg, o, warm);
     if (records || record_offsets) {
       if (!meta || !record_offsets) throw InvalidArgument("packing needs meta and record_offsets");
       PackIn in{c.n_cells, o.K, o.status, o.comps, o.w, o.mu, o.cov};

@@ -238,6 +238,19 @@ __global__ void mt_uniforms_kernel(uint64_t seed, int n, double* out) {
   }
 }
 
+// Per-cell warm-start component counts from a previous results buffer: a cell restarts
+// from its previous model when that fit succeeded, else from the seeded random init.
+__global__ void warm_m_kernel(int n_cells, const int32_t* status, const int32_t* comps, int32_t* m) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n_cells; c += gridDim.x * blockDim.x)
+    m[c] = (!status || status[c] == 0) ? comps[c] : 0;
+}
+
+void launch_warm_m(vdfcg_ctx* ctx, int n_cells, const int32_t* status, const int32_t* comps,
+                   int32_t* m) {
+  const int grid = std::max(1, std::min((n_cells + 255) / 256, ctx->sm_count * 8));
+  VDFCG_LAUNCH(ctx, "warm_m", warm_m_kernel<<<grid, 256, 0, ctx->stream>>>(n_cells, status, comps, m));
+}
+
 void launch_mt_uniforms(vdfcg_ctx* ctx, uint64_t seed, int n, double* out) {
   VDFCG_LAUNCH(ctx, "mt19937_64", mt_uniforms_kernel<<<1, 1, 0, ctx->stream>>>(seed, n, out));
 }
@@ -285,7 +298,7 @@ static int choose_warps(double pts_per_fit, int n_fits, int sm_count) {
 void launch_em_cells(vdfcg_ctx* ctx, int d, const KeyCells& kc, const EmConfig& cfg,
                           const EmOut& out, double avg_particles) {
   if (kc.n_cells == 0) return;
-  const int K = std::max(cfg.M, cfg.warm_m);
+  const int K = std::max(std::max(cfg.M, cfg.warm_m), cfg.cell_warm_m ? cfg.cell_warm_K : 0);
   double bins = 1.0;
   for (int a = 0; a < d; ++a) bins *= kc.n_bins;
   const double est = std::min(bins, avg_particles);

@@ -42,7 +42,16 @@ struct EmConfig {
   const double* warm_cov;
   const double* uniforms;   // [16*3] mt19937_64(seed) uniforms (device)
   unsigned long long* exact_counter;  // optional diagnostics: exact second passes run
+  // Per-cell warm start (time series, pipeline.cpp:482-564): cell c starts from its own
+  // canonical model when cell_warm_m[c] > 0 (else the seeded random init). Device arrays
+  // with component stride cell_warm_K.
+  const int32_t* cell_warm_m;
+  const double* cell_warm_w;
+  const double* cell_warm_mu;
+  const double* cell_warm_cov;
+  int cell_warm_K;
 };
+
 
 struct EmOut {
   int K;
@@ -85,6 +94,10 @@ struct CoordArgs {
 
 // uniforms[0..n) = mt19937_64(seed) top-53-bit doubles (rng.hpp:22), on the device.
 void launch_mt_uniforms(vdfcg_ctx* ctx, uint64_t seed, int n, double* out);
+
+// cell_warm_m[c] = previous status[c] == 0 ? previous components[c] : 0 (device).
+void launch_warm_m(vdfcg_ctx* ctx, int n_cells, const int32_t* status, const int32_t* comps,
+                   int32_t* m);
 
 // Fit every cell of a compacted histogram batch.
 // avg_particles: mean particles per cell (bounds the points per fit for the launch shape).

@@ -229,6 +229,21 @@ VDFCG_DEV void load_cov(const double* c9, Sym3& s) {
   for (int e = 0; e < 9; ++e) s.a[e] = c9[e];
 }
 
+// The init configuration of cell c: its own warm model when the per-cell warm buffers say
+// so (time series), else the shared config (shared warm model or seeded random init).
+template <int D>
+VDFCG_DEV EmConfig cell_config(const EmConfig& cfg, int c) {
+  EmConfig e = cfg;
+  if (cfg.cell_warm_m && cfg.cell_warm_m[c] > 0) {
+    const int64_t base = static_cast<int64_t>(c) * cfg.cell_warm_K;
+    e.warm_m = cfg.cell_warm_m[c];
+    e.warm_w = cfg.cell_warm_w + base;
+    e.warm_mu = cfg.cell_warm_mu + base * D;
+    e.warm_cov = cfg.cell_warm_cov + base * D * D;
+  }
+  return e;
+}
+
 // ---------------------------------------------------------------- the fit
 template <int D, int K, class Src>
 VDFCG_DEV void run_fit(const Src& src, int n, EmState<D, K>& S, double* red, const EmConfig& cfg,
@@ -242,7 +257,10 @@ VDFCG_DEV void run_fit(const Src& src, int n, EmState<D, K>& S, double* red, con
     S.stop = 0;
     S.it_used = 0;
     S.prev_ll = dnan();
-    if (!S.status) S.m = init_model_dev<D>(S.fr, cfg, S.alpha, &S.mu[0][0], &S.cov[0][0]);
+    if (!S.status) {
+      const EmConfig ec = cell_config<D>(cfg, c);
+      S.m = init_model_dev<D>(S.fr, ec, S.alpha, &S.mu[0][0], &S.cov[0][0]);
+    }
   }
   __syncthreads();
 
@@ -497,7 +515,8 @@ VDFCG_DEV int key_prologue(const KeyCells& kc, int c, const EmConfig& cfg, EmSta
     }
   }
   __syncthreads();
-  const bool need_temp = !cfg.has_temp && cfg.warm_m == 0;
+  const bool cell_warm = cfg.warm_m > 0 || (cfg.cell_warm_m && cfg.cell_warm_m[c] > 0);
+  const bool need_temp = !cfg.has_temp && !cell_warm;
   double sw = 0.0, sx[3] = {0, 0, 0}, sxx[3] = {0, 0, 0};
   int mn[3] = {nb, nb, nb}, mxi[3] = {-1, -1, -1};
   for (int p = threadIdx.x; p < n; p += blockDim.x) {
@@ -588,7 +607,7 @@ VDFCG_DEV int key_prologue(const KeyCells& kc, int c, const EmConfig& cfg, EmSta
       if (!S.status) {
         if (cfg.has_temp) {
           for (int a = 0; a < D; ++a) F.temp[a] = cfg.temp[a];
-        } else if (cfg.warm_m == 0) {
+        } else if (!cell_warm) {
           double tsw = 0.0, tsx[3] = {0, 0, 0}, tsxx[3] = {0, 0, 0};
           for (int g = 0; g < G; ++g) {
             tsw += red[g * 8];

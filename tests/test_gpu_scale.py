@@ -155,3 +155,48 @@ def test_cfg4_scale_properties():
         assert struct.unpack("<I", r[hb - 4:hb])[0] == zlib.crc32(r[:hb - 4])
         assert len(r) == hb + m[c] * 80
         assert struct.unpack("<I", r[8:12])[0] == m[c]
+
+
+def _cell_points(bins, offs, c, nb, r, d):
+    """Data-space bin centres of cell c (the oracle's WeightedPoints for that cell)."""
+    k = int(bins.nnz[c])
+    keys = np.asarray(bins.keys[offs[c]:offs[c] + k]).astype(np.int64)
+    idx = []
+    for _ in range(d):
+        idx.append(keys % nb)
+        keys //= nb
+    idx = idx[::-1]
+    pts = np.stack([-r + (i + 0.5) * ((2 * r) / nb) for i in idx], 1)
+    return WeightedPoints(pts, np.asarray(bins.counts[offs[c]:offs[c] + k]).copy(), float(bins.in_range[c]))
+
+
+def test_time_series_warm_start_per_cell():
+    """Per-cell warm start (pipeline.cpp:482-564): cycle 1 fits each cell from its own
+    cycle-0 model; matches the oracle's fit with FitConfig.warm_start = that model
+    (wgmm.cpp:142-161), and static data converges in <= 2 iterations (test_wgmm.cpp:444-479)."""
+    rng = np.random.default_rng(12)
+    n_cells, per = 48, 20000
+    offs = np.arange(n_cells + 1, dtype=np.int64) * per
+    v = rng.normal(size=(n_cells * per, 3))
+    left = rng.random(n_cells * per) < 0.5
+    v[:, 0] += np.where(left, -3.0, 3.0)
+    cfg = FitConfig(initial_components=2, seed=13, temperature=np.ones(3))
+    batch = _batch(v, offs, 24, 6.0)
+    bins0, res0, _, _ = G.compress_cells(batch, cfg)
+    conv = res0.converged.astype(bool)
+    assert conv.sum() >= n_cells // 2
+    # cycle 1, same data: every cell restarts from its own model; converged cells stay put
+    bins1, res1, _, _ = G.compress_cells(batch, cfg, warm=res0)
+    assert (res1.status == 0).all()
+    assert (res1.iterations[conv] <= 2).all(), res1.iterations[conv]
+    # cycle 1 on fresh (drifted) particles: compare against the oracle per cell
+    v2 = v + 0.05 * rng.normal(size=v.shape)
+    b2 = _batch(v2, offs, 24, 6.0)
+    gb, gr, _, _ = G.compress_cells(b2, cfg, warm=res0)
+    assert gr.iterations.mean() < res0.iterations.mean()
+    for c in range(0, n_cells, 6):
+        wp = _cell_points(gb, offs, c, 24, 6.0, 3)
+        fc = FitConfig(initial_components=2, seed=13, temperature=np.ones(3), warm_start=res0.model(c))
+        ro = O.fit(wp, fc)
+        assert gr.iterations[c] == ro.iterations_used
+        assert model_close(gr.model(c), ro.model) <= TOL_EM
