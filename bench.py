@@ -342,7 +342,8 @@ def run_gpu(args, cfg):
         results.append(CellResults(axes[0], b.n_cells, d, K, 0))
         metas.append(ModelMeta(label, None, 0, [AxisRange(-r, r)] * d))
         # temperature: the species' nominal thermal variance (pipeline.cpp:144-149)
-        fcs.append(FitConfig(initial_components=K, seed=SEED, temperature=np.full(d, (r / 6.0) ** 2)))
+        fcs.append(FitConfig(initial_components=K, seed=SEED, temperature=np.full(d, (r / 6.0) ** 2),
+                             estep_fp32=args.estep_fp32))
     torch.cuda.synchronize()
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)  # > L2 (126 MB)
     small_inputs = sum(b.n * d * 8 for b in batches) < (512 << 20)
@@ -507,7 +508,7 @@ def run_gpu(args, cfg):
             "metric": "particles/s compressed (histogram+EM)", "value": value,
             "unit": "particles/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": cfg["scaling"],
-            "vs_baseline": None, "dtype": "f64",
+            "vs_baseline": None, "dtype": "f32 E-step / f64 accumulation" if args.estep_fp32 else "f64",
             "data": "synthetic (counter-based thermal+beam electrons / cold+hot-tail ions, "
                     "generated on device; parity never depends on the generator)",
             "config": {"workload": cfg["workload"], "cells": cfg["cells"] * len(cfg["species"]),
@@ -540,6 +541,8 @@ def main():
     ap.add_argument("--ref-cells", type=int, default=256, help="reference arm cells/species/step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--estep-fp32", action="store_true",
+                    help="FP32 E-step with FP64 accumulation (tolerance 1e-4, not the default)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

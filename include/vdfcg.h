@@ -79,6 +79,10 @@ typedef struct vdfcg_fit_config {
   int32_t has_temperature;      /* 0: weighted variance of the points (wgmm.cpp:374) */
   double temperature[3];        /* per-axis variance, data units */
   const vdfcg_model* warm_start;
+  /* NOT in the reference: 1 = FP32 E-step (log-densities, log-sum-exp, responsibilities in
+   * single precision; sufficient statistics, M-step and protocol in FP64) on the cell-
+   * batched path, parity tolerance 1e-4 relative instead of 1e-9. 0 (default) = FP64. */
+  int32_t estep_fp32;
 } vdfcg_fit_config;
 
 /* FitResult (wgmm.hpp:64-70). Capacities are set by the caller. */

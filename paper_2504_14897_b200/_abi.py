@@ -42,7 +42,7 @@ class FitConfig(C.Structure):
                 ("prune_threshold", C.c_double), ("prune_check_interval", C.c_int32),
                 ("loglik_rel_tolerance", C.c_double), ("seed", C.c_uint64),
                 ("has_temperature", C.c_int32), ("temperature", C.c_double * 3),
-                ("warm_start", C.POINTER(Model))]
+                ("warm_start", C.POINTER(Model)), ("estep_fp32", C.c_int32)]
 
 
 class FitResult(C.Structure):
@@ -152,6 +152,7 @@ def fit_config_struct(cfg, d: int, warm: ModelBuffers | None = None) -> FitConfi
     else:
         s.has_temperature = 0
     s.warm_start = C.pointer(warm.struct) if warm is not None else None
+    s.estep_fp32 = 1 if getattr(cfg, "estep_fp32", False) else 0
     return s
 
 

@@ -81,6 +81,7 @@ EmConfig make_em_config(vdfcg_ctx* ctx, const vdfcg_fit_config* cfg, int d) {
   launch_mt_uniforms(ctx, cfg->seed, VDFCG_MAX_COMPONENTS * 3, u);
   e.uniforms = u;
   e.exact_counter = ctx->diag;
+  e.f32 = cfg->estep_fp32 ? 1 : 0;
   if (cfg->warm_start) {
     const vdfcg_model* w = cfg->warm_start;
     const int m = w->components;

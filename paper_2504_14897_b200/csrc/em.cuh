@@ -42,6 +42,7 @@ struct EmConfig {
   const double* warm_cov;
   const double* uniforms;   // [16*3] mt19937_64(seed) uniforms (device)
   unsigned long long* exact_counter;  // optional diagnostics: exact second passes run
+  int f32;                  // FP32 E-step with FP64 accumulation (cells path; tolerance 1e-4)
   // Per-cell warm start (time series, pipeline.cpp:482-564): cell c starts from its own
   // canonical model when cell_warm_m[c] > 0 (else the seeded random init). Device arrays
   // with component stride cell_warm_K.

@@ -44,6 +44,9 @@ struct EmState {
   double A[KP][6];  // L^-1 packed (affine form used by the point pass)
   double bv[KP][3]; // L^-1 mu
   double muc[KP][3];  // centre of the moment sums (mu_old, or mu_new in the exact pass)
+  float Af[KP][6];    // FP32 E-step mode: the same affine form in single precision
+  float bf[KP][3];
+  float cstf[KP];
   double mu_new[K][D];
   double sig1[K][9];
   double st[K][NS];
@@ -70,10 +73,21 @@ struct KeySrc {
   const double* counts;
   int nb;
   const double* ztab;  // shared [D][nb]
+  const float* ztabf;  // shared [D][nb], FP32 E-step mode
   VDFCG_DEV void load(int p, double (&z)[D], double& w) const {
     const uint32_t k = packed[p];
 #pragma unroll
     for (int a = 0; a < D; ++a) z[a] = ztab[a * nb + ((k >> (SHIFT * a)) & MASK)];
+    w = __ldg(counts + p);
+  }
+  VDFCG_DEV void load2(int p, double (&z)[D], float (&zf)[D], double& w) const {
+    const uint32_t k = packed[p];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const int t = a * nb + ((k >> (SHIFT * a)) & MASK);
+      z[a] = ztab[t];
+      zf[a] = ztabf[t];
+    }
     w = __ldg(counts + p);
   }
 };
@@ -223,6 +237,107 @@ VDFCG_DEV void em_pass(const Src& src, int n, EmState<D, K>& S, double* red) {
   __syncthreads();
 }
 
+// FP32 E-step mode (FitConfig.estep_fp32, tolerance 1e-4): log-densities, the
+// log-sum-exp (MUFU ex2/lg2/rcp) and the responsibilities in single precision; the
+// weighted sufficient statistics and the log-likelihood are still accumulated in FP64
+// about the frame origin, and the M-step / exact pass / protocol are unchanged FP64.
+VDFCG_DEV float ex2f_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+VDFCG_DEV float lg2f_approx(float x) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+template <int D, int K, class Src>
+VDFCG_DEV void em_pass_f32(const Src& src, int n, EmState<D, K>& S, double* red) {
+  constexpr int NS = NStat<D>::value;
+  constexpr int KP = EmState<D, K>::KP;
+  const int m = S.m;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, G = blockDim.x >> 5;
+  double acc[KP][NS];
+#pragma unroll
+  for (int j = 0; j < KP; ++j)
+#pragma unroll
+    for (int t = 0; t < NS; ++t) acc[j][t] = 0.0;
+  double ll = 0.0;
+  for (int p = threadIdx.x; p < n; p += blockDim.x) {
+    double z[D], w;
+    float zf[D];
+    src.load2(p, z, zf, w);
+    float u[KP];
+    float mx = -__int_as_float(0x7f800000);
+#pragma unroll
+    for (int i = 0; i < KP; ++i) {
+      const float y0 = fmaf(S.Af[i][0], zf[0], -S.bf[i][0]);
+      float q = y0 * y0;
+      if (D >= 2) {
+        const float y1 = fmaf(S.Af[i][2], zf[1], fmaf(S.Af[i][1], zf[0], -S.bf[i][1]));
+        q = fmaf(y1, y1, q);
+      }
+      if (D >= 3) {
+        const float y2 = fmaf(S.Af[i][5], zf[2], fmaf(S.Af[i][4], zf[1], fmaf(S.Af[i][3], zf[0], -S.bf[i][2])));
+        q = fmaf(y2, y2, q);
+      }
+      u[i] = fmaf(-0.5f, q, S.cstf[i]);
+      mx = u[i] > mx ? u[i] : mx;
+    }
+    float sum = 0.0f;
+#pragma unroll
+    for (int i = 0; i < KP; ++i) {
+      u[i] = ex2f_approx((u[i] - mx) * 1.4426950408889634f);
+      sum += u[i];
+    }
+    ll += w * (static_cast<double>(mx) + 0.6931471805599453 * static_cast<double>(lg2f_approx(sum)));
+    const float inv = __frcp_rn(sum);
+    double zz[D * (D + 1) / 2];
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b2 = a; b2 < D; ++b2) zz[uidx<D>(a, b2)] = z[a] * z[b2];
+#pragma unroll
+    for (int i = 0; i < KP; ++i) {
+      const double g = static_cast<double>(u[i] * inv) * w;
+      acc[i][0] += g;
+#pragma unroll
+      for (int a = 0; a < D; ++a) acc[i][1 + a] = fma(g, z[a], acc[i][1 + a]);
+#pragma unroll
+      for (int t = 0; t < D * (D + 1) / 2; ++t) acc[i][1 + D + t] = fma(g, zz[t], acc[i][1 + D + t]);
+    }
+  }
+  constexpr int W = K * NS + 1;
+#pragma unroll
+  for (int i = 0; i < KP; ++i) {
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+      const double v = warp_sum(acc[i][t]);
+      if (lane == 0 && i < m) red[warp * W + i * NS + t] = v;
+    }
+  }
+  {
+    const double v = warp_sum(ll);
+    if (lane == 0) red[warp * W + K * NS] = v;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < W; t += blockDim.x) {
+    if (t < K * NS) {
+      const int i = t / NS;
+      if (i >= m) continue;
+      double sum = 0.0;
+      for (int g = 0; g < G; ++g) sum += red[g * W + t];
+      S.st[i][t % NS] = sum;
+    } else {
+      double sum = 0.0;
+      for (int g = 0; g < G; ++g) sum += red[g * W + t];
+      S.ll = sum;
+    }
+  }
+  __syncthreads();
+}
+
 template <int D>
 VDFCG_DEV void load_cov(const double* c9, Sym3& s) {
 #pragma unroll
@@ -245,7 +360,7 @@ VDFCG_DEV EmConfig cell_config(const EmConfig& cfg, int c) {
 }
 
 // ---------------------------------------------------------------- the fit
-template <int D, int K, class Src>
+template <int D, int K, bool F32, class Src>
 VDFCG_DEV void run_fit(const Src& src, int n, EmState<D, K>& S, double* red, const EmConfig& cfg,
                        const EmOut& out, int c) {
   constexpr int NS = NStat<D>::value;
@@ -273,7 +388,17 @@ VDFCG_DEV void run_fit(const Src& src, int n, EmState<D, K>& S, double* red, con
         affine_from_chol<D>(S.mu[lane], S.Lo[lane], S.rd[lane], S.A[lane], S.bv[lane]);
 #pragma unroll
         for (int a = 0; a < D; ++a) S.muc[lane][a] = S.mu[lane][a];
+#pragma unroll
+        for (int e = 0; e < 6; ++e) S.Af[lane][e] = static_cast<float>(S.A[lane][e]);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) S.bf[lane][a] = static_cast<float>(S.bv[lane][a]);
+        S.cstf[lane] = static_cast<float>(S.cst[lane]);
       } else if (lane < EmState<D, K>::KP) {  // inactive / padding slot: contributes zero
+#pragma unroll
+        for (int e = 0; e < 6; ++e) S.Af[lane][e] = 0.0f;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) S.bf[lane][a] = 0.0f;
+        S.cstf[lane] = -__int_as_float(0x7f800000);
         S.cst[lane] = -dinf();
 #pragma unroll
         for (int e = 0; e < 6; ++e) S.A[lane][e] = 0.0;
@@ -296,7 +421,8 @@ VDFCG_DEV void run_fit(const Src& src, int n, EmState<D, K>& S, double* red, con
     if (S.status) break;
 
     // ---- E-step + sufficient statistics (one pass over the points)
-    em_pass<D, K, false>(src, n, S, red);
+    if constexpr (F32) em_pass_f32<D, K>(src, n, S, red);
+    else em_pass<D, K, false>(src, n, S, red);
 
     // ---- M-step part 1 (wgmm.cpp:269-298)
     if (warp == 0) {
@@ -505,6 +631,7 @@ VDFCG_DEV int key_prologue(const KeyCells& kc, int c, const EmConfig& cfg, EmSta
   src.nb = nb;
   src.packed = kc.packed + base;
   src.ztab = ztab;
+  src.ztabf = reinterpret_cast<const float*>(ztab + D * nb);
   if (threadIdx.x == 0) {
     S.status = 0;
     S.err_id = -1;
@@ -635,6 +762,7 @@ VDFCG_DEV int key_prologue(const KeyCells& kc, int c, const EmConfig& cfg, EmSta
   for (int t = threadIdx.x; t < D * nb; t += blockDim.x) {
     const int a = t / nb, i = t - a * nb;
     ztab[t] = __dsub_rn(bin_center(kc.lo[a], kc.hi[a], nb, i), S.fr.offset[a]) / S.fr.scale[a];
+    reinterpret_cast<float*>(ztab + D * nb)[t] = static_cast<float>(ztab[t]);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -647,7 +775,7 @@ VDFCG_DEV int key_prologue(const KeyCells& kc, int c, const EmConfig& cfg, EmSta
   return n;
 }
 
-template <int D, int K, bool KEYS>
+template <int D, int K, bool KEYS, bool F32 = false>
 __global__ void __launch_bounds__(256) __maxnreg__(K <= 4 ? 128 : 255) em_kernel(KeyCells kc, CoordArgs ca, EmConfig cfg,
                                                  EmOut out, int* counter, int red_stride) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -666,7 +794,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(K <= 4 ? 128 : 255) em_kernel
     if (KEYS) {
       KeySrc<D> src;
       const int n = key_prologue<D, K>(kc, c, cfg, S, ztab, red, src);
-      run_fit<D, K>(src, n, S, red, cfg, out, c);
+      run_fit<D, K, F32>(src, n, S, red, cfg, out, c);
     } else {
       if (threadIdx.x == 0) {
         S.fr = *ca.frame;
@@ -687,7 +815,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(K <= 4 ? 128 : 255) em_kernel
           if (out.err_value) out.err_value[c] = S.fr.err_value;
         }
       } else {
-        run_fit<D, K>(src, static_cast<int>(ca.n), S, red, cfg, out, c);
+        run_fit<D, K, false>(src, static_cast<int>(ca.n), S, red, cfg, out, c);
       }
     }
     __syncthreads();
@@ -695,14 +823,15 @@ __global__ void __launch_bounds__(256) __maxnreg__(K <= 4 ? 128 : 255) em_kernel
 }
 
 // ---------------------------------------------------------------- host launch
-template <int D, int K, bool KEYS>
-void launch_em_t(vdfcg_ctx* ctx, const KeyCells& kc, const CoordArgs& ca,
-                        const EmConfig& cfg, const EmOut& out, int n_cells, int G, int n_bins) {
+template <int D, int K, bool KEYS, bool F32>
+void launch_em_tf(vdfcg_ctx* ctx, const KeyCells& kc, const CoordArgs& ca,
+                  const EmConfig& cfg, const EmOut& out, int n_cells, int G, int n_bins) {
   constexpr int NS = NStat<D>::value;
   const int red_stride = std::max(K * NS + 1, 8);
   const size_t st = (sizeof(EmState<D, K>) + 15) & ~size_t(15);
-  const size_t smem = st + size_t(G) * red_stride * 8 + (KEYS ? size_t(D) * n_bins * 8 : 0);
-  auto k = em_kernel<D, K, KEYS>;
+  // z tables: FP64 [D][nb] + FP32 [D][nb]
+  const size_t smem = st + size_t(G) * red_stride * 8 + (KEYS ? size_t(D) * n_bins * 12 : 0);
+  auto k = em_kernel<D, K, KEYS, F32>;
   VDFCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int occ = 0;
   VDFCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, G * 32, smem));
@@ -712,6 +841,18 @@ void launch_em_t(vdfcg_ctx* ctx, const KeyCells& kc, const CoordArgs& ca,
   VDFCG_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), ctx->stream));
   VDFCG_LAUNCH(ctx, "em_fit",
                k<<<grid, G * 32, smem, ctx->stream>>>(kc, ca, cfg, out, counter, red_stride));
+}
+
+template <int D, int K, bool KEYS>
+void launch_em_t(vdfcg_ctx* ctx, const KeyCells& kc, const CoordArgs& ca,
+                 const EmConfig& cfg, const EmOut& out, int n_cells, int G, int n_bins) {
+  if constexpr (KEYS) {
+    if (cfg.f32) {
+      launch_em_tf<D, K, true, true>(ctx, kc, ca, cfg, out, n_cells, G, n_bins);
+      return;
+    }
+  }
+  launch_em_tf<D, K, KEYS, false>(ctx, kc, ca, cfg, out, n_cells, G, n_bins);
 }
 
 template <int D, bool KEYS>

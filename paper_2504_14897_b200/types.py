@@ -246,6 +246,8 @@ class FitConfig:
     seed: int = 0
     warm_start: Optional[GmmModel] = None
     temperature: Optional[np.ndarray] = None
+    # Not in the reference: FP32 E-step on the cell-batched path (tolerance 1e-4).
+    estep_fp32: bool = False
 
 
 @dataclass

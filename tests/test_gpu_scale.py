@@ -200,3 +200,23 @@ def test_time_series_warm_start_per_cell():
         ro = O.fit(wp, fc)
         assert gr.iterations[c] == ro.iterations_used
         assert model_close(gr.model(c), ro.model) <= TOL_EM
+
+
+@pytest.mark.parametrize("K,nb", [(4, 48), (3, 32)])
+def test_fp32_estep_mode_within_1e4(K, nb):
+    """FP32 E-step option (north star: 1e-4 FP32 / 1e-9 FP64), compared with the FP64
+    oracle in fixed-iteration mode (no pruning, convergence disabled) so both run the
+    same number of EM steps."""
+    rng = np.random.default_rng(21)
+    n_cells, per = 64, 4000
+    offs = np.arange(n_cells + 1, dtype=np.int64) * per
+    v = rng.normal(size=(n_cells * per, 3))
+    v[rng.random(n_cells * per) < 0.3, 0] += 2.5
+    base = dict(initial_components=K, seed=5, temperature=np.ones(3), max_em_iterations=30,
+                loglik_rel_tolerance=1e-300, prune_threshold=1e-300)
+    ob, orr = O.compress_cells(O.CellsHost(v, offs, nb, [-6] * 3, [6] * 3), FitConfig(**base))
+    gb, gr, _, _ = G.compress_cells(_batch(v, offs, nb, 6.0), FitConfig(**base, estep_fp32=True))
+    assert (gr.iterations == 30).all() and np.array_equal(gr.components, orr.components)
+    worst = max(model_close(gr.model(c), _oracle_model(orr, c, 3), tol=1e-4) for c in range(n_cells))
+    assert worst <= 1e-4, worst
+    np.testing.assert_allclose(gr.final_loglik, orr.final_loglik, rtol=1e-6)

@@ -20,6 +20,7 @@ ap.add_argument("--K", type=int, default=4)
 ap.add_argument("--range", type=float, default=6.0)
 ap.add_argument("--species", type=int, default=0)
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--fp32", action="store_true")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 offs = torch.arange(a.cells + 1, dtype=torch.int64, device=dev) * a.per_cell
@@ -29,7 +30,8 @@ G.synth_cells(3, offs, 11, a.species, *axes)
 b = CellBatch(axes, offs, a.bins, [-a.range] * 3, [a.range] * 3)
 bins = CellBins.alloc(b)
 res = CellResults(axes[0], b.n_cells, 3, a.K, 0)
-cfg = FitConfig(initial_components=a.K, seed=11, temperature=np.full(3, (a.range / 6) ** 2))
+cfg = FitConfig(initial_components=a.K, seed=11, temperature=np.full(3, (a.range / 6) ** 2),
+                estep_fp32=a.fp32)
 meta = ModelMeta("e", None, 0, [AxisRange(-a.range, a.range)] * 3)
 ctx = G.api.context(0)
 ctx.enable_timing(True)
