@@ -734,7 +734,8 @@ static bool any_host(const std::vector<std::function<void()>>& fin) { return !fi
 
 static void fit_cells_dev(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& b,
                           const vdfcg_fit_config* cfg, const EmOut& o,
-                          const vdfcg_cell_results* warm = nullptr) {
+                          const vdfcg_cell_results* warm = nullptr,
+                          uint32_t* packed_scratch = nullptr) {
   const int kw = warm ? warm->capacity_components : 0;
   if (warm && (kw < 1 || kw > VDFCG_MAX_COMPONENTS))
     throw InvalidArgument("warm cell results must have capacity_components in 1..16");
@@ -764,14 +765,15 @@ static void fit_cells_dev(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& 
   kc.keys = b.keys;
   kc.counts = b.counts;
   kc.in_range = b.in_range;
-  kc.packed = arena<uint32_t>(ctx, size_t(std::max<int64_t>(c.n, 1)));
+  // decoded-bin scratch, indexed by absolute particle offsets (full batch)
+  kc.packed = packed_scratch ? packed_scratch : arena<uint32_t>(ctx, size_t(std::max<int64_t>(c.n, 1)));
   kc.n_bins = c.n_bins;
   for (int a = 0; a < 3; ++a) {
     kc.lo[a] = c.lo[a];
     kc.hi[a] = c.hi[a];
   }
-  const double avg = c.n_cells ? double(c.n) / c.n_cells : 0.0;
-  launch_em_cells(ctx, c.d, kc, e, o, avg);
+  const double avg = c.shape_cells > 0 ? c.shape_avg : c.n_cells ? double(c.n) / c.n_cells : 0.0;
+  launch_em_cells(ctx, c.d, kc, e, o, avg, c.shape_cells);
 }
 
 int vdfcg_bin_cells(vdfcg_ctx* ctx, const vdfcg_cells* cells, vdfcg_cell_bins* out) {
@@ -870,6 +872,174 @@ int vdfcg_compress_cells(vdfcg_ctx* ctx, const vdfcg_cells* cells, const vdfcg_f
                                    record_offsets);
 }
 
+// Sub-batch views of cells [c0, c1): the kernels index particles through cell_offsets,
+// so only the per-cell arrays are offset.
+static CellsDev sub_cells(const CellsDev& c, int c0, int c1) {
+  CellsDev s = c;
+  s.offsets = c.offsets + c0;
+  s.n_cells = c1 - c0;
+  return s;
+}
+static CellBinsDev sub_bins(const CellBinsDev& b, int c0) {
+  CellBinsDev s = b;
+  s.nnz += c0;
+  s.oor += c0;
+  s.in_range += c0;
+  return s;
+}
+static EmOut sub_out(const EmOut& o, int c0, int d) {
+  EmOut s = o;
+  const int64_t K = o.K;
+  s.status += c0;
+  s.comps += c0;
+  s.iters += c0;
+  s.conv += c0;
+  s.final_ll += c0;
+  s.w += c0 * K;
+  s.mu += c0 * K * d;
+  s.cov += c0 * K * d * d;
+  if (s.trace) s.trace += int64_t(c0) * o.trace_cap;
+  if (s.n_events) {
+    s.n_events += c0;
+    s.ev_it += c0 * K;
+    s.ev_comp += c0 * K;
+    s.ev_w += c0 * K;
+  }
+  return s;
+}
+static vdfcg_cell_results sub_warm(const vdfcg_cell_results& w, int c0, int d) {
+  vdfcg_cell_results s = w;
+  const int64_t K = w.capacity_components;
+  if (s.status) s.status += c0;
+  s.components += c0;
+  s.weights += c0 * K;
+  s.means += c0 * K * d;
+  s.covariances += c0 * K * d * d;
+  return s;
+}
+
+static void pack_into(vdfcg_ctx* ctx, const CellsDev& c, const EmOut& o,
+                      const vdfcg_model_meta* meta, uint8_t* records, int64_t capacity,
+                      int64_t* record_offsets, std::vector<std::function<void()>>& fin) {
+  if (!records && !record_offsets) return;
+  if (!meta || !record_offsets) throw InvalidArgument("packing needs meta and record_offsets");
+  PackIn in{c.n_cells, o.K, o.status, o.comps, o.w, o.mu, o.cov};
+  PackMeta pm = make_pack_meta(ctx, meta, c.d);
+  auto offs = stage_out(ctx, record_offsets, size_t(c.n_cells) + 1);
+  const int64_t total = launch_pack_offsets(ctx, in, pm, offs.dev);
+  if (total > capacity) throw InvalidArgument("compress_cells: record capacity too small");
+  auto rec = stage_out(ctx, records, size_t(total));
+  if (total) launch_pack(ctx, in, pm, offs.dev, rec.dev);
+  fin.push_back([=] {
+    finish(ctx, offs);
+    finish(ctx, rec);
+  });
+}
+
+// Host-resident particles: the velocity (and weight) ranges of successive cell chunks are
+// copied on the context's copy stream while the compute stream bins and fits the chunks
+// already resident, so the end-to-end time approaches max(H2D, compute) instead of the sum.
+static bool compress_pipelined(vdfcg_ctx* ctx, const vdfcg_cells* cells,
+                               const vdfcg_fit_config* cfg, const vdfcg_cell_results* warm,
+                               vdfcg_cell_bins* bins, vdfcg_cell_results* out,
+                               const vdfcg_model_meta* meta, uint8_t* records, int64_t capacity,
+                               int64_t* record_offsets) {
+  const int d = cells->dimension;
+  if (d != 2 && d != 3) return false;
+  if (cells->n_particles < (int64_t(1) << 22) || cells->n_cells < 4) return false;
+  for (int a = 0; a < d; ++a)
+    if (!cells->velocity[a] || is_device_pointer(cells->velocity[a])) return false;
+  if (is_device_pointer(cells->cell_offsets)) return false;
+  if (cells->weights && is_device_pointer(cells->weights)) return false;
+  // malformed offsets take the staged path, whose device checks raise the usual error
+  const int64_t* ho = cells->cell_offsets;
+  if (!ho || ho[0] < 0 || ho[cells->n_cells] > cells->n_particles) return false;
+  for (int q = 0; q < cells->n_cells; ++q)
+    if (ho[q + 1] < ho[q]) return false;
+  // validation identical to stage_cells, without the bulk copies
+  if (cells->n_bins < 2) throw InvalidArgument("n_bins must be >= 2");
+  double nbd = 1.0;
+  for (int a = 0; a < d; ++a) nbd *= cells->n_bins;
+  if (nbd > 2147483647.0) throw InvalidArgument("n_bins^d must fit a 31-bit bin key");
+  if (d == 3 && cells->n_bins > 1024) throw InvalidArgument("3V cells support n_bins <= 1024");
+  for (int a = 0; a < d; ++a)
+    if (!range_ok(cells->lo[a], cells->hi[a]))
+      throw InvalidArgument("axis range must satisfy min < max");
+  const int64_t n = cells->n_particles;
+  const int nc = cells->n_cells;
+  const int64_t* hoff = cells->cell_offsets;
+  CellsDev c{};
+  c.d = d;
+  c.n = n;
+  c.n_cells = nc;
+  c.n_bins = cells->n_bins;
+  for (int a = 0; a < 3; ++a) {
+    c.lo[a] = cells->lo[a];
+    c.hi[a] = cells->hi[a];
+  }
+  c.offsets = stage_in(ctx, hoff, size_t(nc) + 1).dev;
+  double* dv[3] = {nullptr, nullptr, nullptr};
+  for (int a = 0; a < d; ++a) dv[a] = arena<double>(ctx, size_t(n));
+  double* dw = cells->weights ? arena<double>(ctx, size_t(n)) : nullptr;
+  for (int a = 0; a < 3; ++a) c.vel[a] = a < d ? dv[a] : dv[0];
+  c.w = dw;
+  // chunks of ~equal particle counts, whole cells
+  const int nch = std::min(16, nc);
+  std::vector<int> bounds{0};
+  for (int j = 1; j < nch; ++j) {
+    const int64_t target = hoff[0] + (hoff[nc] - hoff[0]) * j / nch;
+    const int cb = static_cast<int>(std::upper_bound(hoff, hoff + nc + 1, target) - hoff) - 1;
+    bounds.push_back(std::max(bounds.back(), std::min(cb, nc)));
+  }
+  bounds.push_back(nc);
+  // the copy stream starts after everything already queued on the compute stream
+  cudaEvent_t start;
+  VDFCG_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  VDFCG_CUDA(cudaEventRecord(start, ctx->stream));
+  VDFCG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, start, 0));
+  std::vector<cudaEvent_t> ready(bounds.size() - 1);
+  for (size_t j = 0; j + 1 < bounds.size(); ++j) {
+    const int64_t p0 = hoff[bounds[j]], p1 = hoff[bounds[j + 1]];
+    const size_t bytes = size_t(p1 - p0) * sizeof(double);
+    if (bytes) {
+      for (int a = 0; a < d; ++a)
+        VDFCG_CUDA(cudaMemcpyAsync(dv[a] + p0, cells->velocity[a] + p0, bytes,
+                                   cudaMemcpyHostToDevice, ctx->copy_stream));
+      if (dw)
+        VDFCG_CUDA(cudaMemcpyAsync(dw + p0, cells->weights + p0, bytes, cudaMemcpyHostToDevice,
+                                   ctx->copy_stream));
+    }
+    VDFCG_CUDA(cudaEventCreateWithFlags(&ready[j], cudaEventDisableTiming));
+    VDFCG_CUDA(cudaEventRecord(ready[j], ctx->copy_stream));
+  }
+  validate_config(cfg, d);
+  std::vector<std::function<void()>> fin;
+  CellBinsDev b = bins_dev(ctx, c, bins, fin);
+  EmOut o = results_dev(ctx, nc, d, out, fin);
+  uint32_t* packed = arena<uint32_t>(ctx, size_t(n));
+  for (size_t j = 0; j + 1 < bounds.size(); ++j) {
+    const int c0 = bounds[j], c1 = bounds[j + 1];
+    VDFCG_CUDA(cudaStreamWaitEvent(ctx->stream, ready[j], 0));
+    if (c1 <= c0) continue;
+    CellsDev sc = sub_cells(c, c0, c1);
+    sc.n = hoff[c1] - hoff[c0];  // this chunk's particles (histogram launch shapes)
+    sc.max_cell = 0;             // known on the host: no device round trip per chunk
+    for (int q = c0; q < c1; ++q) sc.max_cell = std::max(sc.max_cell, hoff[q + 1] - hoff[q]);
+    sc.shape_cells = nc;         // EM launch shape of the whole batch (bitwise-identical results)
+    sc.shape_avg = double(hoff[nc] - hoff[0]) / nc;
+    launch_bin_cells(ctx, sc, sub_bins(b, c0));
+    vdfcg_cell_results sw{};
+    if (warm) sw = sub_warm(*warm, c0, d);
+    fit_cells_dev(ctx, sc, sub_bins(b, c0), cfg, sub_out(o, c0, d), warm ? &sw : nullptr, packed);
+  }
+  pack_into(ctx, c, o, meta, records, capacity, record_offsets, fin);
+  for (auto& f : fin) f();
+  sync(ctx);
+  cudaEventDestroy(start);
+  for (auto e : ready) cudaEventDestroy(e);
+  return true;
+}
+
 int vdfcg_compress_cells_warm(vdfcg_ctx* ctx, const vdfcg_cells* cells,
                               const vdfcg_fit_config* cfg, const vdfcg_cell_results* warm,
                               vdfcg_cell_bins* bins, vdfcg_cell_results* out,
@@ -877,6 +1047,10 @@ int vdfcg_compress_cells_warm(vdfcg_ctx* ctx, const vdfcg_cells* cells,
                               int64_t* record_offsets) {
   return guard_impl([&] {
     begin(ctx);
+    if (!cells) throw InvalidArgument("null cells");
+    if (compress_pipelined(ctx, cells, cfg, warm, bins, out, meta, records, capacity,
+                           record_offsets))
+      return;
     CellsDev c = stage_cells(ctx, cells);
     validate_config(cfg, c.d);
     std::vector<std::function<void()>> fin;
@@ -884,20 +1058,7 @@ int vdfcg_compress_cells_warm(vdfcg_ctx* ctx, const vdfcg_cells* cells,
     EmOut o = results_dev(ctx, c.n_cells, c.d, out, fin);
     launch_bin_cells(ctx, c, b);
     fit_cells_dev(ctx, c, b, cfg, o, warm);
-    if (records || record_offsets) {
-      if (!meta || !record_offsets) throw InvalidArgument("packing needs meta and record_offsets");
-      PackIn in{c.n_cells, o.K, o.status, o.comps, o.w, o.mu, o.cov};
-      PackMeta pm = make_pack_meta(ctx, meta, c.d);
-      auto offs = stage_out(ctx, record_offsets, size_t(c.n_cells) + 1);
-      const int64_t total = launch_pack_offsets(ctx, in, pm, offs.dev);
-      if (total > capacity) throw InvalidArgument("compress_cells: record capacity too small");
-      auto rec = stage_out(ctx, records, size_t(total));
-      if (total) launch_pack(ctx, in, pm, offs.dev, rec.dev);
-      fin.push_back([=] {
-        finish(ctx, offs);
-        finish(ctx, rec);
-      });
-    }
+    pack_into(ctx, c, o, meta, records, capacity, record_offsets, fin);
     for (auto& f : fin) f();
     if (any_host(fin)) sync(ctx);
   });

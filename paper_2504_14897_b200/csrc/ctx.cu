@@ -148,6 +148,7 @@ int vdfcg_ctx_create(int device, vdfcg_ctx** out) {
     c->sm_count = prop.multiProcessorCount;
     c->smem_optin = prop.sharedMemPerBlockOptin;
     VDFCG_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+    VDFCG_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     c->stream = c->own_stream;
     VDFCG_CUDA(cudaHostAlloc(&c->pinned, 4096, cudaHostAllocDefault));
     VDFCG_CUDA(cudaMalloc(&c->diag, 8 * sizeof(unsigned long long)));
@@ -169,6 +170,10 @@ int vdfcg_ctx_destroy(vdfcg_ctx* ctx) {
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->diag) cudaFree(ctx->diag);
+    if (ctx->copy_stream) {
+      cudaStreamSynchronize(ctx->copy_stream);
+      cudaStreamDestroy(ctx->copy_stream);
+    }
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
   });

@@ -43,6 +43,7 @@ struct vdfcg_ctx {
   size_t smem_optin = 0;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // H2D of later cell chunks overlaps compute
   // grow-only arena, reset at the start of every API call
   struct Chunk {
     char* base;

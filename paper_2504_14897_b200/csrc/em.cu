@@ -296,13 +296,13 @@ static int choose_warps(double pts_per_fit, int n_fits, int sm_count) {
 }
 
 void launch_em_cells(vdfcg_ctx* ctx, int d, const KeyCells& kc, const EmConfig& cfg,
-                          const EmOut& out, double avg_particles) {
+                          const EmOut& out, double avg_particles, int shape_fits) {
   if (kc.n_cells == 0) return;
   const int K = std::max(std::max(cfg.M, cfg.warm_m), cfg.cell_warm_m ? cfg.cell_warm_K : 0);
   double bins = 1.0;
   for (int a = 0; a < d; ++a) bins *= kc.n_bins;
   const double est = std::min(bins, avg_particles);
-  const int G = choose_warps(est, kc.n_cells, ctx->sm_count);
+  const int G = choose_warps(est, shape_fits > 0 ? shape_fits : kc.n_cells, ctx->sm_count);
   CoordArgs ca{};
   if (d == 2) launch_em_dim2(ctx, true, K, kc, ca, cfg, out, kc.n_cells, G, kc.n_bins);
   else launch_em_dim3(ctx, true, K, kc, ca, cfg, out, kc.n_cells, G, kc.n_bins);

@@ -101,9 +101,11 @@ void launch_warm_m(vdfcg_ctx* ctx, int n_cells, const int32_t* status, const int
                    int32_t* m);
 
 // Fit every cell of a compacted histogram batch.
-// avg_particles: mean particles per cell (bounds the points per fit for the launch shape).
+// avg_particles: mean particles per cell (bounds the points per fit for the launch shape);
+// shape_fits: number of fits the shape is chosen for (0 = kc.n_cells). Chunked calls pass
+// the whole batch's figures so every chunk runs the launch shape the whole batch would.
 void launch_em_cells(vdfcg_ctx* ctx, int d, const KeyCells& kc, const EmConfig& cfg,
-                     const EmOut& out, double avg_particles);
+                     const EmOut& out, double avg_particles, int shape_fits = 0);
 
 // Fit one set of explicit points (N x d column-major, data space) — vdfcg_fit.
 void launch_em_points(vdfcg_ctx* ctx, int d, const double* pts, const double* w, int64_t n,

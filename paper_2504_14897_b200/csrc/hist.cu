@@ -751,7 +751,7 @@ static void bin_cells_d(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
   const bool weighted = c.w != nullptr;
   int* err = arena<int>(ctx, 1);
   VDFCG_CUDA(cudaMemsetAsync(err, 0, sizeof(int), ctx->stream));
-  const int64_t maxc = max_cell_size(ctx, c.offsets, c.n_cells);
+  const int64_t maxc = c.max_cell >= 0 ? c.max_cell : max_cell_size(ctx, c.offsets, c.n_cells);
   const double avg = c.n_cells ? double(c.n) / c.n_cells : 0.0;
   const int binbits = bits_for(static_cast<uint64_t>(bins));  // SENT = 2^binbits - 1 > any bin
   // Sparse cells: unit weights use the occupancy bitmap (no sort); fractional weights

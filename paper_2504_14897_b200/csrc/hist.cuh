@@ -29,6 +29,9 @@ struct CellsDev {
   const int64_t* offsets;
   int n_bins;
   double lo[3], hi[3];
+  int64_t max_cell = -1;   // largest cell, when the host already knows it (else computed)
+  int shape_cells = 0;     // EM launch shape from the whole batch when > 0 (chunked calls)
+  double shape_avg = 0.0;
 };
 struct CellBinsDev {
   int32_t* nnz;

@@ -220,3 +220,30 @@ def test_fp32_estep_mode_within_1e4(K, nb):
     worst = max(model_close(gr.model(c), _oracle_model(orr, c, 3), tol=1e-4) for c in range(n_cells))
     assert worst <= 1e-4, worst
     np.testing.assert_allclose(gr.final_loglik, orr.final_loglik, rtol=1e-6)
+
+
+def test_pipelined_host_path_bitwise_equals_device_path():
+    """Host-resident inputs take the chunked H2D/compute-overlap path; results and .gmmc
+    records must be bitwise identical to the device-resident path."""
+    import torch
+    dev = torch.device("cuda", 0)
+    n_cells, per = 4096, 1500
+    offs = torch.arange(n_cells + 1, dtype=torch.int64, device=dev) * per
+    axes = [torch.empty(n_cells * per, dtype=torch.float64, device=dev) for _ in range(3)]
+    G.synth_cells(3, offs, 7, 0, *axes)
+    cfg = FitConfig(initial_components=4, seed=11, temperature=np.ones(3))
+    meta = ModelMeta("e", None, 3, [AxisRange(-6, 6)] * 3)
+    _, rd, recd, offd = G.compress_cells(G.CellBatch(axes, offs, 48, [-6] * 3, [6] * 3), cfg, meta)
+    host_axes = [a.cpu().pin_memory() for a in axes]
+    hb = G.CellBatch(host_axes, offs.cpu(), 48, [-6] * 3, [6] * 3)
+    _, rh, rech, offh = G.compress_cells(hb, cfg, meta)
+    assert torch.equal(recd.cpu(), rech) and torch.equal(offd.cpu(), offh)
+    for f in ("status", "components", "iterations", "weights", "means", "covariances", "final_loglik"):
+        a, b = getattr(rd, f).cpu(), getattr(rh, f)
+        if a.dtype == torch.float64:  # compare bit patterns
+            a, b = a.view(torch.int64), b.view(torch.int64)
+        if f in ("weights", "means", "covariances"):  # slots past `components` are unspecified
+            a, b = a.view(n_cells, 4, -1), b.view(n_cells, 4, -1)
+            used = torch.arange(4)[None, :] < rh.components[:, None].long()
+            a, b = a[used], b[used]
+        assert torch.equal(a, b), f
