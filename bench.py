@@ -455,7 +455,7 @@ def run_gpu(args, cfg):
             of = b.offsets.cpu().pin_memory()
             host.append(CellBatch(ax, of, b.n_bins, b.lo, b.hi))
             h2d += sum(a.numel() * 8 for a in ax) + of.numel() * 8
-        hres = [CellResults(np.zeros(1), b.n_cells, d, K, 0) for b in batches]
+        hres = [CellResults(torch.empty(1).pin_memory(), b.n_cells, d, K, 0) for b in batches]
         torch.cuda.synchronize()
         d2h = [0]
 

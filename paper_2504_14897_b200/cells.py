@@ -36,7 +36,9 @@ def _empty(like, shape, kind: str):
         import torch
         dt = {"f64": torch.float64, "i32": torch.int32, "u32": torch.int32, "i64": torch.int64,
               "u8": torch.uint8}[kind]
-        return torch.empty(shape, dtype=dt, device=like.device)
+        # host outputs follow the input's pinnedness (pinned D2H is asynchronous + faster)
+        pin = like.device.type == "cpu" and like.is_pinned()
+        return torch.empty(shape, dtype=dt, device=like.device, pin_memory=pin)
     dt = {"f64": np.float64, "i32": np.int32, "u32": np.uint32, "i64": np.int64, "u8": np.uint8}[kind]
     return np.empty(shape, dtype=dt)
 

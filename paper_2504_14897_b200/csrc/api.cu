@@ -735,7 +735,7 @@ static bool any_host(const std::vector<std::function<void()>>& fin) { return !fi
 static void fit_cells_dev(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& b,
                           const vdfcg_fit_config* cfg, const EmOut& o,
                           const vdfcg_cell_results* warm = nullptr,
-                          uint32_t* packed_scratch = nullptr) {
+                          uint32_t* packed_scratch = nullptr, const EmConfig* prebuilt = nullptr) {
   const int kw = warm ? warm->capacity_components : 0;
   if (warm && (kw < 1 || kw > VDFCG_MAX_COMPONENTS))
     throw InvalidArgument("warm cell results must have capacity_components in 1..16");
@@ -743,7 +743,7 @@ static void fit_cells_dev(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& 
     throw InvalidArgument("cell results capacity_components too small");
   if (o.trace_cap && o.trace_cap < cfg->max_em_iterations)
     throw InvalidArgument("cell results capacity_trace too small");
-  EmConfig e = make_em_config(ctx, cfg, c.d);
+  EmConfig e = prebuilt ? *prebuilt : make_em_config(ctx, cfg, c.d);
   if (warm) {  // per-cell warm start from a previous (device or host) results buffer
     const size_t nc = c.n_cells;
     const int32_t* st = warm->status ? stage_in(ctx, warm->status, nc).dev : nullptr;
@@ -983,11 +983,14 @@ static bool compress_pipelined(vdfcg_ctx* ctx, const vdfcg_cells* cells,
   double* dw = cells->weights ? arena<double>(ctx, size_t(n)) : nullptr;
   for (int a = 0; a < 3; ++a) c.vel[a] = a < d ? dv[a] : dv[0];
   c.w = dw;
-  // chunks of ~equal particle counts, whole cells
+  // whole-cell chunks; the first two are small (1/64, then 3/64 of the particles) so
+  // compute starts early, the rest are equal
   const int nch = std::min(16, nc);
   std::vector<int> bounds{0};
   for (int j = 1; j < nch; ++j) {
-    const int64_t target = hoff[0] + (hoff[nc] - hoff[0]) * j / nch;
+    const double f = nch < 16 ? double(j) / nch
+                     : j == 1 ? 1.0 / 64 : 1.0 / 16 + (15.0 / 16) * (j - 2) / (nch - 2);
+    const int64_t target = hoff[0] + static_cast<int64_t>(double(hoff[nc] - hoff[0]) * f);
     const int cb = static_cast<int>(std::upper_bound(hoff, hoff + nc + 1, target) - hoff) - 1;
     bounds.push_back(std::max(bounds.back(), std::min(cb, nc)));
   }
@@ -1017,21 +1020,43 @@ static bool compress_pipelined(vdfcg_ctx* ctx, const vdfcg_cells* cells,
   CellBinsDev b = bins_dev(ctx, c, bins, fin);
   EmOut o = results_dev(ctx, nc, d, out, fin);
   uint32_t* packed = arena<uint32_t>(ctx, size_t(n));
-  for (size_t j = 0; j + 1 < bounds.size(); ++j) {
-    const int c0 = bounds[j], c1 = bounds[j + 1];
-    VDFCG_CUDA(cudaStreamWaitEvent(ctx->stream, ready[j], 0));
-    if (c1 <= c0) continue;
-    CellsDev sc = sub_cells(c, c0, c1);
-    sc.n = hoff[c1] - hoff[c0];  // this chunk's particles (histogram launch shapes)
-    sc.max_cell = 0;             // known on the host: no device round trip per chunk
-    for (int q = c0; q < c1; ++q) sc.max_cell = std::max(sc.max_cell, hoff[q + 1] - hoff[q]);
-    sc.shape_cells = nc;         // EM launch shape of the whole batch (bitwise-identical results)
-    sc.shape_avg = double(hoff[nc] - hoff[0]) / nc;
-    launch_bin_cells(ctx, sc, sub_bins(b, c0));
-    vdfcg_cell_results sw{};
-    if (warm) sw = sub_warm(*warm, c0, d);
-    fit_cells_dev(ctx, sc, sub_bins(b, c0), cfg, sub_out(o, c0, d), warm ? &sw : nullptr, packed);
+  const EmConfig em = make_em_config(ctx, cfg, d);  // mt19937_64 uniforms once per call
+  // Chunks alternate between the context stream and the aux stream so one chunk's fits
+  // start while the previous chunk's last fits drain. Every fit is independent, so the
+  // results do not depend on the interleaving.
+  cudaStream_t main = ctx->stream;
+  cudaEvent_t fork, join;
+  VDFCG_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+  VDFCG_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+  VDFCG_CUDA(cudaEventRecord(fork, main));
+  VDFCG_CUDA(cudaStreamWaitEvent(ctx->aux_stream, fork, 0));
+  try {
+    for (size_t j = 0; j + 1 < bounds.size(); ++j) {
+      const int c0 = bounds[j], c1 = bounds[j + 1];
+      if (c1 <= c0) continue;
+      ctx->stream = (j & 1) ? ctx->aux_stream : main;
+      VDFCG_CUDA(cudaStreamWaitEvent(ctx->stream, ready[j], 0));
+      CellsDev sc = sub_cells(c, c0, c1);
+      sc.n = hoff[c1] - hoff[c0];  // this chunk's particles (histogram launch shapes)
+      sc.max_cell = 0;             // known on the host: no device round trip per chunk
+      for (int q = c0; q < c1; ++q) sc.max_cell = std::max(sc.max_cell, hoff[q + 1] - hoff[q]);
+      sc.shape_cells = nc;         // EM launch shape of the whole batch (bitwise-identical results)
+      sc.shape_avg = double(hoff[nc] - hoff[0]) / nc;
+      launch_bin_cells(ctx, sc, sub_bins(b, c0));
+      vdfcg_cell_results sw{};
+      if (warm) sw = sub_warm(*warm, c0, d);
+      fit_cells_dev(ctx, sc, sub_bins(b, c0), cfg, sub_out(o, c0, d), warm ? &sw : nullptr, packed,
+                    &em);
+    }
+  } catch (...) {
+    ctx->stream = main;
+    throw;
   }
+  ctx->stream = main;
+  VDFCG_CUDA(cudaEventRecord(join, ctx->aux_stream));
+  VDFCG_CUDA(cudaStreamWaitEvent(main, join, 0));
+  cudaEventDestroy(fork);
+  cudaEventDestroy(join);
   pack_into(ctx, c, o, meta, records, capacity, record_offsets, fin);
   for (auto& f : fin) f();
   sync(ctx);

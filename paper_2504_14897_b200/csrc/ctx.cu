@@ -149,6 +149,7 @@ int vdfcg_ctx_create(int device, vdfcg_ctx** out) {
     c->smem_optin = prop.sharedMemPerBlockOptin;
     VDFCG_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
     VDFCG_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    VDFCG_CUDA(cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
     c->stream = c->own_stream;
     VDFCG_CUDA(cudaHostAlloc(&c->pinned, 4096, cudaHostAllocDefault));
     VDFCG_CUDA(cudaMalloc(&c->diag, 8 * sizeof(unsigned long long)));
@@ -170,6 +171,10 @@ int vdfcg_ctx_destroy(vdfcg_ctx* ctx) {
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->diag) cudaFree(ctx->diag);
+    if (ctx->aux_stream) {
+      cudaStreamSynchronize(ctx->aux_stream);
+      cudaStreamDestroy(ctx->aux_stream);
+    }
     if (ctx->copy_stream) {
       cudaStreamSynchronize(ctx->copy_stream);
       cudaStreamDestroy(ctx->copy_stream);
