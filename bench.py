@@ -496,12 +496,26 @@ def run_gpu(args, cfg):
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
         gmap = {s: res_np[s] for s in range(len(batches))} if c0 == 0 else None
-        rate, frate, sec, sp, sf, parity = cpu_oracle_rate(cfg, args.cpu_cells, threads, gmap)
+        # median of `cpu_repeats` runs on all host threads, plus one
+        # single-thread run on a smaller subset
+        runs = []
+        for r in range(max(1, args.cpu_repeats)):
+            out = cpu_oracle_rate(cfg, args.cpu_cells, threads, gmap if r == 0 else None)
+            if r == 0:
+                parity = out[5]
+            runs.append(out)
+        runs.sort(key=lambda o: o[0])
+        rate, frate, sec, sp, sf, _ = runs[len(runs) // 2]
+        r1 = cpu_oracle_rate(cfg, max(1, args.cpu_cells // 16), 1)
         cpu = {"value": rate, "unit": "particles/s", "cores": threads, "kind": "port",
-               "fits_per_s": frate, "seconds": sec,
-               "sample": f"{int(sf)} cells ({int(sp)} particles): every "
+               "fits_per_s": frate, "seconds": sec, "repeats": len(runs),
+               "values_all_repeats": [o[0] for o in runs],
+               "single_core_value": r1[0], "single_core_fits_per_s": r1[1],
+               "single_core_sample": f"{int(r1[4])} cells ({int(r1[3])} particles), 1 thread",
+               "sample": f"{int(sf)} cells ({int(sp)} particles) per repeat: every "
                          f"{cfg['cells'] // max(args.cpu_cells, 1)}th cell of each species, "
-                         "bin+compact+fit per cell on a thread pool (oracle/ C++ restatement)"}
+                         "bin+compact+fit per cell on a thread pool (oracle/ C++ restatement); "
+                         "value = median over repeats"}
 
     if rank == 0:
         line = {
@@ -537,7 +551,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-cells", type=int, default=512, help="CPU-baseline sample cells/species")
+    ap.add_argument("--cpu-cells", type=int, default=2048, help="CPU-baseline sample cells/species")
+    ap.add_argument("--cpu-repeats", type=int, default=3, help="CPU-baseline repeats (median)")
     ap.add_argument("--ref-cells", type=int, default=256, help="reference arm cells/species/step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -280,6 +280,45 @@ int vdfcg_pack_cells(vdfcg_ctx* ctx, int32_t n_cells, int32_t dimension,
                      const vdfcg_cell_results* res, const vdfcg_model_meta* meta,
                      uint8_t* records, int64_t capacity, int64_t* record_offsets);
 
+/* ---- Fit quality ------------------------------------------- */
+
+/* Per-cell MetricsReport (metrics.hpp:39-54) as assemble_metrics computes it
+ * (pipeline.cpp:106-128), over each cell's bins^d grid: d = 2 is the reference's plane
+ * case, d = 3 applies the same formulas to the 3V grid. Arrays are [n_cells]; any may be
+ * NULL. Cells with status != 0, no components or an empty histogram get NaN. `cells`
+ * supplies the grid (n_bins, lo, hi), cell_offsets (bins CSR + raw particle counts) and
+ * dimension; its particle arrays are not read. */
+typedef struct vdfcg_cell_metrics {
+  double* jsd;                 /* metrics.cpp:28-46, clamped to [0, ln 2] */
+  double* kl_pq;               /* metrics.cpp:12-26, D(hist || model); +inf = divergent */
+  double* kl_qp;               /* D(model || hist) */
+  double* loglik;              /* weighted_loglik (wgmm.cpp:257-267) over the cell's points */
+  double* bic;                 /* metrics.cpp:52-56 with n = total weight */
+  double* bic_bin_count;       /* ... with n = n_bins^d */
+  double* mean_moment_error;   /* metrics.cpp:58-65 */
+  double* second_moment_error;
+  double* compression_ratio_vs_histogram;  /* n_bins^d * 8 / payload bytes */
+  double* compression_ratio_vs_raw;        /* cell particles * d * 8 / payload bytes */
+} vdfcg_cell_metrics;
+
+int vdfcg_metrics_cells(vdfcg_ctx* ctx, const vdfcg_cells* cells, const vdfcg_cell_bins* bins,
+                        const vdfcg_cell_results* res, vdfcg_cell_metrics* out);
+
+/* evaluate_pdf (wgmm.hpp:130, wgmm.cpp:425-453): d = 2 model (normalisation map honoured)
+ * on the n_bins x n_bins grid; out column-major, out(i,j) at i + j*n_bins. */
+int vdfcg_evaluate_pdf(vdfcg_ctx* ctx, const vdfcg_model* model, int32_t n_bins, double xlo,
+                       double xhi, double ylo, double yhi, double* out);
+
+/* weighted_loglik (wgmm.cpp:257-267): sum_n w_n log sum_k alpha_k N(x_n), points N x d
+ * column-major; covariances are repaired on a copy like the reference. */
+int vdfcg_weighted_loglik(vdfcg_ctx* ctx, const vdfcg_model* model, const double* points,
+                          const double* weights, int64_t n, double* out);
+
+/* kl_divergence / jsd (metrics.cpp:12-46) of two aligned normalised grids of n values
+ * (PdfGrid values; bin mass = value * area). Any output may be NULL. */
+int vdfcg_pdf_divergences(vdfcg_ctx* ctx, const double* p, const double* q, int64_t n,
+                          double area, double* jsd, double* kl_pq, double* kl_qp);
+
 /* The whole compression step: bin_cells -> fit_cells (-> pack_cells when records != NULL),
  * one stream, no host round trip in between. */
 int vdfcg_compress_cells(vdfcg_ctx* ctx, const vdfcg_cells* cells, const vdfcg_fit_config* cfg,

@@ -18,7 +18,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(_HERE))
 
-from paper_2504_14897_b200 import _abi, _marshal  # noqa: E402
+from paper_2504_14897_b200 import _abi, _marshal, _metrics  # noqa: E402
 from paper_2504_14897_b200.types import (AxisRange, FitConfig, ParticleSet,  # noqa: E402,F401
                                          WeightedPoints)
 
@@ -74,6 +74,13 @@ _lib.oracle_weighted_data_moments.argtypes = [C.c_void_p, C.c_void_p, C.c_int64,
 _lib.oracle_bin_cells.argtypes = [C.c_void_p, C.c_void_p]
 _lib.oracle_compress_cells.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                        C.c_void_p, C.c_void_p]
+_lib.oracle_evaluate_pdf.argtypes = [C.c_void_p, C.c_int32, C.c_double, C.c_double, C.c_double,
+                                     C.c_double, C.c_void_p]
+_lib.oracle_weighted_loglik.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
+_lib.oracle_pdf_divergences.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_double, C.c_void_p,
+                                        C.c_void_p, C.c_void_p]
+_lib.oracle_cell_metrics.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
+                                     C.c_int32, C.c_void_p]
 _lib.oracle_pack_cells.argtypes = [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_int64, C.c_void_p]
 
@@ -265,6 +272,35 @@ def pack_cells(res: CellResultsHost, n_cells: int, meta) -> tuple[bytes, np.ndar
     _marshal.check(_lib.oracle_pack_cells(n_cells, res.d, C.byref(res.struct), C.byref(ms),
                                           buf.ctypes.data, cap, offs.ctypes.data), _err)
     return buf[:offs[-1]].tobytes(), offs
+
+
+# ----------------------------------------------------------------- fit quality
+evaluate_pdf = partial(_metrics.evaluate_pdf, _call, _err)
+weighted_loglik = partial(_metrics.weighted_loglik, _call, _err)
+kl_divergence = partial(_metrics.kl_divergence, _call, _err)
+jsd = partial(_metrics.jsd, _call, _err)
+assemble_metrics = partial(_metrics.assemble_metrics, _call, _err)
+from paper_2504_14897_b200._metrics import (MetricsReport, PdfGrid, bic,  # noqa: E402,F401
+                                            bic_parameter_count, compression_ratio,
+                                            moment_errors, to_pdf)
+
+
+class CellMetricsHost:
+    def __init__(self, n_cells: int):
+        for f in _abi.METRIC_FIELDS:
+            setattr(self, f, np.zeros(n_cells))
+        self.struct = _abi.CellMetrics(*[getattr(self, f).ctypes.data for f in _abi.METRIC_FIELDS])
+
+
+def cell_metrics(cells: CellsHost, bins: CellBinsHost, res: CellResultsHost, cell_begin: int = 0,
+                 cell_end: int | None = None, threads: int = 0) -> CellMetricsHost:
+    """pipeline.cpp:106-128 assemble_metrics for every cell."""
+    out = CellMetricsHost(cells.n_cells)
+    end = cells.n_cells if cell_end is None else cell_end
+    _marshal.check(_lib.oracle_cell_metrics(C.byref(cells.struct), C.byref(bins.struct),
+                                            C.byref(res.struct), cell_begin, end, threads,
+                                            C.byref(out.struct)), _err)
+    return out
 
 
 # ----------------------------------------------------------------- reference refem

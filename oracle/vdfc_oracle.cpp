@@ -904,6 +904,151 @@ std::vector<uint8_t> encode_impl(const Model& model, const vdfcg_model_meta* met
   return out;
 }
 
+// ---- fit quality ----------------------------------------------------------
+// gaussian.hpp:22-28 log_gaussian through the Eigen-order Cholesky factor.
+double log_gaussian(const double* z, const double* mu, const Mat3& L, int d) {
+  double y[3];
+  for (int a = 0; a < d; ++a) {
+    double v = z[a] - mu[a];
+    for (int b = 0; b < a; ++b) v -= L[a][b] * y[b];
+    y[a] = v / L[a][a];
+  }
+  double ld = 0.0;
+  for (int k = 0; k < d; ++k) ld += std::log(L[k][k]);
+  double sq = 0.0;
+  for (int a = 0; a < d; ++a) sq += y[a] * y[a];
+  return -0.5 * (d * std::log(2.0 * M_PI) + 2.0 * ld + sq);
+}
+
+// wgmm.cpp:425-453 evaluate_pdf over the bins^d grid in flat key order (i*n+j)*n+k.
+void evaluate_grid(const Model& m, int nb, const double* lo, const double* hi,
+                   std::vector<double>& out) {
+  validate_model(m);
+  const int d = m.d;
+  std::vector<Mat3> L(m.c.size());
+  for (size_t k = 0; k < m.c.size(); ++k)
+    if (!cholesky(m.c[k].cov, d, L[k])) throw std::runtime_error("model component covariance is not SPD");
+  double vol = 1.0;
+  if (m.has_map)
+    for (int a = 0; a < d; ++a) vol *= m.scale[a];
+  const double inv_vol = 1.0 / vol;
+  int64_t total = 1;
+  for (int a = 0; a < d; ++a) total *= nb;
+  out.assign(total, 0.0);
+  for (int64_t key = 0; key < total; ++key) {
+    int64_t r = key;
+    double z[3];
+    for (int a = d - 1; a >= 0; --a) {
+      const int i = static_cast<int>(r % nb);
+      r /= nb;
+      const double x = center(lo[a], hi[a], nb, i);
+      z[a] = m.has_map ? (x - m.offset[a]) / m.scale[a] : x;
+    }
+    double p = 0.0;
+    for (size_t k = 0; k < m.c.size(); ++k) p += m.c[k].w * std::exp(log_gaussian(z, m.c[k].mu, L[k], d));
+    out[key] = p * inv_vol;
+  }
+}
+
+// pdf_grid.cpp:5-19 PdfGrid::normalized
+void normalize_grid(std::vector<double>& v, double area) {
+  double s = 0.0;
+  for (double x : v) {
+    if (x < 0.0) throw std::invalid_argument("pdf grid values must be non-negative");
+    s += x;
+  }
+  const double total = s * area;
+  if (!(total > 0.0) || !std::isfinite(total))
+    throw std::invalid_argument("degenerate pdf grid: total mass is zero or non-finite");
+  for (double& x : v) x /= total;
+}
+
+// metrics.cpp:12-26 kl_divergence
+double kl_impl(const double* p, const double* q, int64_t n, double area) {
+  double sum = 0.0;
+  for (int64_t b = 0; b < n; ++b) {
+    const double pn = p[b] * area;
+    if (!(pn > 0.0)) continue;
+    const double qn = q[b] * area;
+    if (!(qn > 0.0)) return kInf;
+    sum += pn * std::log(pn / qn);
+  }
+  return sum;
+}
+
+// metrics.cpp:28-46 jsd (out of [0, ln 2] beyond 1e-9 -> the reference throws logic_error)
+double jsd_impl(const double* p, const double* q, int64_t n, double area) {
+  double sum = 0.0;
+  for (int64_t b = 0; b < n; ++b) {
+    const double pn = p[b] * area;
+    const double qn = q[b] * area;
+    const double mn = 0.5 * (pn + qn);
+    if (pn > 0.0) sum += 0.5 * pn * std::log(pn / mn);
+    if (qn > 0.0) sum += 0.5 * qn * std::log(qn / mn);
+  }
+  constexpr double ln2 = 0.6931471805599453;
+  if (sum < -1e-9 || sum > ln2 + 1e-9)
+    throw std::logic_error("jsd outside [0, ln 2] beyond numerical slack");
+  return std::clamp(sum, 0.0, ln2);
+}
+
+// wgmm.cpp:257-267 weighted_loglik
+double weighted_loglik_impl(const Model& model, const Points& p) {
+  Model scratch = model.identity() ? model : denormalize_impl(model);
+  std::vector<double> logp;
+  log_component_densities(scratch, p, logp, nullptr);
+  const int M = static_cast<int>(scratch.c.size());
+  Kahan ll;
+  for (int64_t n = 0; n < p.n; ++n) {
+    double mx = -kInf;
+    for (int i = 0; i < M; ++i) mx = std::max(mx, logp[i + n * M]);
+    double s = 0.0;
+    for (int i = 0; i < M; ++i) s += std::exp(logp[i + n * M] - mx);
+    ll.add(p.w[n] * (mx + std::log(s)));
+  }
+  return ll.s;
+}
+
+// wgmm.cpp:455-471 mixture_moments (identity or mapped model)
+void mixture_moments_impl(const Model& m, double* mean, double* m2) {
+  const int d = m.d;
+  double mu[3] = {0, 0, 0}, s2[9] = {0};
+  for (const Comp& c : m.c) {
+    for (int a = 0; a < d; ++a) mu[a] += c.w * c.mu[a];
+    for (int a = 0; a < d; ++a)
+      for (int b = 0; b < d; ++b) s2[a * d + b] += c.w * (c.cov[a][b] + c.mu[a] * c.mu[b]);
+  }
+  if (m.identity()) {
+    std::copy(mu, mu + d, mean);
+    std::copy(s2, s2 + d * d, m2);
+    return;
+  }
+  for (int a = 0; a < d; ++a) mean[a] = mu[a] * m.scale[a] + m.offset[a];
+  for (int a = 0; a < d; ++a)
+    for (int b = 0; b < d; ++b)
+      m2[a * d + b] = m.scale[a] * s2[a * d + b] * m.scale[b] + m.scale[a] * mu[a] * m.offset[b] +
+                      m.offset[a] * (m.scale[b] * mu[b]) + m.offset[a] * m.offset[b];
+}
+
+// metrics.cpp:58-65 moment_errors
+void moment_errors_impl(const Model& m, const Points& p, double* mean_err, double* m2_err) {
+  const int d = m.d;
+  double mm[3], m2[9], dm[3], d2[9];
+  mixture_moments_impl(m, mm, m2);
+  data_moments(p, dm, d2);
+  double tr = 0.0, num = 0.0, n2 = 0.0, dn = 0.0;
+  for (int a = 0; a < d; ++a) tr += d2[a * d + a];
+  for (int a = 0; a < d; ++a) num += (mm[a] - dm[a]) * (mm[a] - dm[a]);
+  for (int e = 0; e < d * d; ++e) {
+    n2 += (m2[e] - d2[e]) * (m2[e] - d2[e]);
+    dn += d2[e] * d2[e];
+  }
+  *mean_err = std::sqrt(num) / std::sqrt(tr);
+  *m2_err = std::sqrt(n2) / std::sqrt(dn);
+}
+
+int64_t payload_bytes(int M, int d) { return static_cast<int64_t>(M) * (1 + d + d * (d + 1) / 2) * 8; }
+
 }  // namespace
 
 // ===========================================================================
@@ -1258,6 +1403,120 @@ int oracle_pack_cells(int32_t n_cells, int32_t d, const vdfcg_cell_results* res,
       }
       offsets[c + 1] = pos;
     }
+  });
+}
+
+int oracle_evaluate_pdf(const vdfcg_model* model, int32_t nb, double xlo, double xhi, double ylo,
+                        double yhi, double* out) {
+  return guarded([&] {
+    const Model m = from_view(model);
+    if (m.d != 2) throw std::invalid_argument("evaluate_pdf expects a 2-dimensional model");
+    if (!(nb >= 1) || !(xlo < xhi) || !(ylo < yhi) || !std::isfinite(xlo) || !std::isfinite(xhi) ||
+        !std::isfinite(ylo) || !std::isfinite(yhi))
+      throw std::invalid_argument("invalid grid spec");
+    const double lo[2] = {xlo, ylo}, hi[2] = {xhi, yhi};
+    std::vector<double> g;
+    evaluate_grid(m, nb, lo, hi, g);
+    for (int i = 0; i < nb; ++i)
+      for (int j = 0; j < nb; ++j) out[i + static_cast<int64_t>(j) * nb] = g[static_cast<int64_t>(i) * nb + j];
+  });
+}
+
+int oracle_weighted_loglik(const vdfcg_model* model, const double* points, const double* weights,
+                           int64_t n, double* out) {
+  return guarded([&] {
+    const Model m = from_view(model);
+    Points p = make_points(points, weights, n, m.d, 0.0);
+    *out = weighted_loglik_impl(m, p);
+  });
+}
+
+int oracle_pdf_divergences(const double* p, const double* q, int64_t n, double area, double* jsd,
+                           double* kl_pq, double* kl_qp) {
+  return guarded([&] {
+    if (kl_pq) *kl_pq = kl_impl(p, q, n, area);
+    if (kl_qp) *kl_qp = kl_impl(q, p, n, area);
+    if (jsd) *jsd = jsd_impl(p, q, n, area);
+  });
+}
+
+int oracle_cell_metrics(const vdfcg_cells* cells, const vdfcg_cell_bins* bins,
+                        const vdfcg_cell_results* res, int32_t cell_begin, int32_t cell_end,
+                        int32_t threads, vdfcg_cell_metrics* out) {
+  return guarded([&] {
+    const int d = cells->dimension;
+    const int nb = cells->n_bins;
+    const int K = res->capacity_components;
+    if (threads <= 0) threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+    std::atomic<int> next{cell_begin};
+    auto put = [](double* a, int c, double v) {
+      if (a) a[c] = v;
+    };
+    auto worker = [&] {
+      std::vector<double> hist, model;
+      for (;;) {
+        const int c = next.fetch_add(1);
+        if (c >= cell_end) break;
+        double v[10];
+        std::fill(v, v + 10, kNaN);
+        const int M = res->components[c];
+        if (res->status[c] == VDFCG_OK && M > 0 && bins->in_range[c] > 0.0) {
+          try {
+            Model m;
+            m.d = d;
+            m.c.resize(M);
+            for (int i = 0; i < M; ++i) {
+              m.c[i].w = res->weights[c * K + i];
+              for (int a = 0; a < d; ++a) m.c[i].mu[a] = res->means[(c * K + i) * d + a];
+              for (int a = 0; a < d; ++a)
+                for (int b = 0; b < d; ++b)
+                  m.c[i].cov[a][b] = res->covariances[((c * K + i) * d + a) * d + b];
+            }
+            double area = 1.0;
+            int64_t total = 1;
+            for (int a = 0; a < d; ++a) {
+              area *= (cells->hi[a] - cells->lo[a]) / nb;
+              total *= nb;
+            }
+            const int64_t b0 = cells->cell_offsets[c];
+            hist.assign(total, 0.0);
+            for (int r = 0; r < bins->nnz[c]; ++r) hist[bins->keys[b0 + r]] = bins->counts[b0 + r];
+            normalize_grid(hist, area);  // to_pdf (histogram.cpp:111-115)
+            evaluate_grid(m, nb, cells->lo, cells->hi, model);
+            normalize_grid(model, area);
+            v[0] = jsd_impl(hist.data(), model.data(), total, area);
+            v[1] = kl_impl(hist.data(), model.data(), total, area);
+            v[2] = kl_impl(model.data(), hist.data(), total, area);
+            const Points p = cell_points(cells, c, bins->keys, bins->counts, bins->nnz[c], bins->in_range[c]);
+            const double ll = weighted_loglik_impl(m, p);
+            const double k = static_cast<double>(M * (1 + d * (d + 3) / 2));
+            v[3] = ll;
+            v[4] = -2.0 * ll + k * std::log(p.total);
+            v[5] = -2.0 * ll + k * std::log(static_cast<double>(total));
+            moment_errors_impl(m, p, &v[6], &v[7]);
+            const double mb = static_cast<double>(payload_bytes(M, d));
+            v[8] = static_cast<double>(total * 8) / mb;
+            v[9] = static_cast<double>((cells->cell_offsets[c + 1] - b0) * d * 8) / mb;
+          } catch (const std::exception&) {
+            std::fill(v, v + 10, kNaN);
+          }
+        }
+        put(out->jsd, c, v[0]);
+        put(out->kl_pq, c, v[1]);
+        put(out->kl_qp, c, v[2]);
+        put(out->loglik, c, v[3]);
+        put(out->bic, c, v[4]);
+        put(out->bic_bin_count, c, v[5]);
+        put(out->mean_moment_error, c, v[6]);
+        put(out->second_moment_error, c, v[7]);
+        put(out->compression_ratio_vs_histogram, c, v[8]);
+        put(out->compression_ratio_vs_raw, c, v[9]);
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < threads; ++t) pool.emplace_back(worker);
+    worker();
+    for (auto& t : pool) t.join();
   });
 }
 

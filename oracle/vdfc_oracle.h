@@ -94,6 +94,21 @@ int oracle_pack_cells(int32_t n_cells, int32_t dimension, const vdfcg_cell_resul
                       const vdfcg_model_meta* meta, uint8_t* records, int64_t capacity,
                       int64_t* record_offsets);
 
+/* wgmm.cpp:425-453 evaluate_pdf (d = 2): out n x n column-major, out(i,j) at i + j*n. */
+int oracle_evaluate_pdf(const vdfcg_model* model, int32_t n_bins, double xlo, double xhi,
+                        double ylo, double yhi, double* out);
+/* wgmm.cpp:257-267 weighted_loglik (repair on a copy; Kahan over points). */
+int oracle_weighted_loglik(const vdfcg_model* model, const double* points, const double* weights,
+                           int64_t n, double* out);
+/* metrics.cpp:12-46 over two aligned normalised grids of n values (any layout, same order). */
+int oracle_pdf_divergences(const double* p, const double* q, int64_t n, double area,
+                           double* jsd, double* kl_pq, double* kl_qp);
+/* pipeline.cpp:106-128 assemble_metrics per cell over the bins^d grid (d = 2 is the
+ * reference's plane case; d = 3 the same formulas over the 3V grid). */
+int oracle_cell_metrics(const vdfcg_cells* cells, const vdfcg_cell_bins* bins,
+                        const vdfcg_cell_results* res, int32_t cell_begin, int32_t cell_end,
+                        int32_t threads, vdfcg_cell_metrics* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -81,6 +81,15 @@ class CellResults(C.Structure):
                 ("event_weight", C.c_void_p)]
 
 
+METRIC_FIELDS = ("jsd", "kl_pq", "kl_qp", "loglik", "bic", "bic_bin_count", "mean_moment_error",
+                 "second_moment_error", "compression_ratio_vs_histogram",
+                 "compression_ratio_vs_raw")
+
+
+class CellMetrics(C.Structure):
+    _fields_ = [(f, C.c_void_p) for f in METRIC_FIELDS]
+
+
 def header_functions(path: str = HEADER) -> list[str]:
     """Names of every function the C-ABI header declares."""
     text = open(path).read()

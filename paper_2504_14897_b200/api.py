@@ -14,7 +14,7 @@ from functools import partial
 
 import numpy as np
 
-from . import _abi, _marshal
+from . import _abi, _marshal, _metrics
 from .types import (AxisRange, FitConfig, GmmModel, InvalidArgument, ModelMeta,  # noqa: F401
                     ParticleSet, WeightedPoints)
 
@@ -61,6 +61,10 @@ def _bind(lib) -> None:
         "vdfcg_compress_cells_warm": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, i64, vp]),
         "vdfcg_synth_cells": (C.c_int, [vp, i32, i32, vp, i64, u64, i32, vp, vp, vp]),
         "vdfcg_probe_peaks": (C.c_int, [vp, vp, vp]),
+        "vdfcg_metrics_cells": (C.c_int, [vp, vp, vp, vp, vp]),
+        "vdfcg_evaluate_pdf": (C.c_int, [vp, vp, i32, f64, f64, f64, f64, vp]),
+        "vdfcg_weighted_loglik": (C.c_int, [vp, vp, vp, vp, i64, vp]),
+        "vdfcg_pdf_divergences": (C.c_int, [vp, vp, vp, i64, f64, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -186,6 +190,16 @@ fit = partial(_marshal.fit, _call, _err)
 encode_model = partial(_marshal.encode_model, _call, _err)
 model_payload_bytes = _marshal.model_payload_bytes
 
+# fit quality (metrics.hpp, wgmm.hpp:128-136)
+evaluate_pdf = partial(_metrics.evaluate_pdf, _call, _err)
+weighted_loglik = partial(_metrics.weighted_loglik, _call, _err)
+kl_divergence = partial(_metrics.kl_divergence, _call, _err)
+jsd = partial(_metrics.jsd, _call, _err)
+assemble_metrics = partial(_metrics.assemble_metrics, _call, _err)
+from ._metrics import (MetricsReport, PdfGrid, bic, bic_parameter_count,  # noqa: E402,F401
+                       compression_ratio, mixture_moments, moment_errors, to_pdf,
+                       weighted_data_moments)
+
 
 def default_axis_range(particles: ParticleSet, axis: int) -> AxisRange:
     """histogram.cpp:27-30: +/- 5 nominal thermal speeds."""
@@ -206,5 +220,5 @@ def validate_fit_config(config: FitConfig, d: int) -> None:
     _marshal.check(lib().vdfcg_validate_fit_config(C.byref(cfg), d), last_error)
 
 
-from .cells import (CellBatch, bin_cells, compress_cells, fit_cells, pack_cells,  # noqa: E402,F401
-                    synth_cells)
+from .cells import (CellBatch, CellMetrics, bin_cells, cell_metrics,  # noqa: E402,F401
+                    compress_cells, fit_cells, pack_cells, synth_cells)

@@ -249,6 +249,39 @@ def compress_cells(batch: CellBatch, config: FitConfig, meta: Optional[ModelMeta
     return bins, results, rec, offs
 
 
+class CellMetrics:
+    """Per-cell MetricsReport fields (vdfcg_cell_metrics), one array per field."""
+
+    FIELDS = _abi.METRIC_FIELDS
+
+    def __init__(self, like, n_cells: int):
+        self.n_cells = n_cells
+        for f in self.FIELDS:
+            setattr(self, f, _empty(like, (n_cells,), "f64"))
+
+    def struct(self) -> _abi.CellMetrics:
+        return _abi.CellMetrics(*[_ptr(getattr(self, f)) for f in self.FIELDS])
+
+    def report(self, c: int):
+        """Cell c as a MetricsReport (metrics.hpp:39-54)."""
+        from ._metrics import MetricsReport
+        vals = {f: float(getattr(self, f)[c]) for f in MetricsReport.FIELDS}
+        return MetricsReport(**vals)
+
+
+def cell_metrics(batch: CellBatch, bins: CellBins, results: CellResults,
+                 out: Optional[CellMetrics] = None) -> CellMetrics:
+    """assemble_metrics (pipeline.cpp:106-128) for every cell, on the device: JSD and both
+    KL divergences between the cell histogram and the model pdf on the bins^d grid,
+    weighted log-likelihood, BIC (both n's), moment errors, compression ratios."""
+    api = _api()
+    out = out or CellMetrics(batch.axes[0], batch.n_cells)
+    bs, rs, ms = bins.struct(), results.struct(), out.struct()
+    _check(api.lib().vdfcg_metrics_cells(api.context().handle, C.byref(batch.struct), C.byref(bs),
+                                         C.byref(rs), C.byref(ms)))
+    return out
+
+
 def synth_cells(d: int, cell_offsets, seed: int, species: int, u, v, w=None,
                 cell_base: int = 0) -> None:
     """Deterministic synthetic plasma cells into device tensors (tests/bench data).

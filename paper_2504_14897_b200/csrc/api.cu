@@ -13,6 +13,7 @@
 #include "em.cuh"
 #include "em_entry.cuh"
 #include "hist.cuh"
+#include "metrics.cuh"
 #include "pack.cuh"
 
 namespace vdfcg {
@@ -1086,6 +1087,157 @@ int vdfcg_compress_cells_warm(vdfcg_ctx* ctx, const vdfcg_cells* cells,
     pack_into(ctx, c, o, meta, records, capacity, record_offsets, fin);
     for (auto& f : fin) f();
     if (any_host(fin)) sync(ctx);
+  });
+}
+
+// ---- fit quality --------------------------------------------
+// GmmModel::validate (wgmm.cpp:46-63) on the device, then the staged model.
+static ModelDev staged_valid_model(vdfcg_ctx* ctx, const vdfcg_model* model) {
+  if (!model) throw InvalidArgument("null model");
+  const int d = model->dimension, m = model->components;
+  if (d < 1) throw InvalidArgument("model dimension must be positive");
+  if (m < 1) throw InvalidArgument("model has no components");
+  if (d > 3) throw InvalidArgument("model dimension must be <= 3");
+  if (m > VDFCG_MAX_COMPONENTS) throw InvalidArgument("model has more than 16 components");
+  auto w = stage_in(ctx, model->weights, m);
+  auto mu = stage_in(ctx, model->means, size_t(m) * d);
+  auto cv = stage_in(ctx, model->covariances, size_t(m) * d * d);
+  int* code = arena<int>(ctx, 1);
+  VDFCG_LAUNCH(ctx, "validate_model", validate_model_kernel<<<1, 32, 0, ctx->stream>>>(d, m, w.dev, cv.dev, code));
+  const int c = read_scalar(ctx, code);
+  if (c == 2) throw InvalidArgument("component weight must be > 0");
+  if (c == 3) throw InvalidArgument("component covariance is not symmetric");
+  if (c == 4) throw InvalidArgument("component weights must sum to 1");
+  ModelDev md{d, m, w.dev, mu.dev, cv.dev, nullptr, nullptr};
+  if (model->scale && model->offset) {
+    md.scale = stage_in(ctx, model->scale, d).dev;
+    md.offset = stage_in(ctx, model->offset, d).dev;
+  }
+  return md;
+}
+
+int vdfcg_metrics_cells(vdfcg_ctx* ctx, const vdfcg_cells* cells, const vdfcg_cell_bins* bins,
+                        const vdfcg_cell_results* res, vdfcg_cell_metrics* out) {
+  return guard_impl([&] {
+    begin(ctx);
+    if (!cells || !bins || !res || !out) throw InvalidArgument("null argument");
+    const int d = cells->dimension;
+    if (d != 2 && d != 3) throw InvalidArgument("particle dimension must be 2 or 3");
+    if (cells->n_bins < 2) throw InvalidArgument("n_bins must be >= 2");
+    for (int a = 0; a < d; ++a)
+      if (!range_ok(cells->lo[a], cells->hi[a])) throw InvalidArgument("axis range must satisfy min < max");
+    if (cells->n_cells < 0 || cells->n_particles < 0) throw InvalidArgument("negative sizes");
+    if (!cells->cell_offsets) throw InvalidArgument("cell_offsets is required");
+    const int K = res->capacity_components;
+    if (K < 1 || K > VDFCG_MAX_COMPONENTS) throw InvalidArgument("capacity_components must be 1..16");
+    if (!bins->nnz || !bins->keys || !bins->counts || !bins->in_range)
+      throw InvalidArgument("cell bins: nnz, keys, counts and in_range are required");
+    if (!res->status || !res->components || !res->weights || !res->means || !res->covariances)
+      throw InvalidArgument("cell results: status, components, weights, means, covariances are required");
+    const size_t nc = cells->n_cells, n = cells->n_particles;
+    CellsDev c{};
+    c.d = d;
+    c.n = cells->n_particles;
+    c.n_cells = cells->n_cells;
+    c.n_bins = cells->n_bins;
+    for (int a = 0; a < 3; ++a) {
+      c.lo[a] = cells->lo[a];
+      c.hi[a] = cells->hi[a];
+    }
+    c.offsets = stage_in(ctx, cells->cell_offsets, nc + 1).dev;
+    CellBinsDev b{};
+    b.nnz = const_cast<int32_t*>(stage_in(ctx, bins->nnz, nc).dev);
+    b.keys = const_cast<uint32_t*>(stage_in(ctx, bins->keys, n).dev);
+    b.counts = const_cast<double*>(stage_in(ctx, bins->counts, n).dev);
+    b.in_range = const_cast<double*>(stage_in(ctx, bins->in_range, nc).dev);
+    CellModels r{K,
+                 stage_in(ctx, res->status, nc).dev,
+                 stage_in(ctx, res->components, nc).dev,
+                 stage_in(ctx, res->weights, nc * K).dev,
+                 stage_in(ctx, res->means, nc * K * d).dev,
+                 stage_in(ctx, res->covariances, nc * K * d * d).dev};
+    double* fields[kMetricFields] = {out->jsd, out->kl_pq, out->kl_qp, out->loglik, out->bic,
+                                     out->bic_bin_count, out->mean_moment_error,
+                                     out->second_moment_error, out->compression_ratio_vs_histogram,
+                                     out->compression_ratio_vs_raw};
+    MetricsOut mo{};
+    std::vector<Staged<double>> st;
+    for (int f = 0; f < kMetricFields; ++f) {
+      st.push_back(stage_out(ctx, fields[f], fields[f] ? nc : 0));
+      mo.f[f] = st.back().dev;
+    }
+    launch_cell_metrics(ctx, c, b, r, mo);
+    bool host = false;
+    for (auto& x : st) {
+      finish(ctx, x);
+      host = host || x.staged;
+    }
+    if (host) sync(ctx);
+  });
+}
+
+int vdfcg_evaluate_pdf(vdfcg_ctx* ctx, const vdfcg_model* model, int32_t n_bins, double xlo,
+                       double xhi, double ylo, double yhi, double* out) {
+  return guard_impl([&] {
+    begin(ctx);
+    if (!out) throw InvalidArgument("null output");
+    ModelDev m = staged_valid_model(ctx, model);
+    if (m.d != 2) throw InvalidArgument("evaluate_pdf expects a 2-dimensional model");
+    if (n_bins < 1 || !range_ok(xlo, xhi) || !range_ok(ylo, yhi)) throw InvalidArgument("invalid grid spec");
+    auto o = stage_out(ctx, out, size_t(n_bins) * n_bins);
+    int* err = arena<int>(ctx, 1);
+    VDFCG_CUDA(cudaMemsetAsync(err, 0, sizeof(int), ctx->stream));
+    const double lo[2] = {xlo, ylo}, hi[2] = {xhi, yhi};
+    launch_evaluate_pdf(ctx, m, n_bins, lo, hi, o.dev, err);
+    if (read_scalar(ctx, err)) throw RuntimeError("model component covariance is not SPD");
+    finish(ctx, o);
+    sync(ctx);
+  });
+}
+
+int vdfcg_weighted_loglik(vdfcg_ctx* ctx, const vdfcg_model* model, const double* points,
+                          const double* weights, int64_t n, double* out) {
+  return guard_impl([&] {
+    begin(ctx);
+    if (!model || !out) throw InvalidArgument("null argument");
+    const int d = model->dimension, m = model->components;
+    if (d != 2 && d != 3) throw InvalidArgument("model dimension must be 2 or 3");
+    if (m < 1 || m > VDFCG_MAX_COMPONENTS) throw InvalidArgument("model components must be 1..16");
+    if (n < 0 || (n > 0 && (!points || !weights))) throw InvalidArgument("null points");
+    ModelDev md{d, m, stage_in(ctx, model->weights, m).dev, stage_in(ctx, model->means, size_t(m) * d).dev,
+                stage_in(ctx, model->covariances, size_t(m) * d * d).dev, nullptr, nullptr};
+    if (model->scale && model->offset) {
+      md.scale = stage_in(ctx, model->scale, d).dev;
+      md.offset = stage_in(ctx, model->offset, d).dev;
+    }
+    const double* px = stage_in(ctx, points, size_t(n) * d).dev;
+    const double* pw = stage_in(ctx, weights, size_t(n)).dev;
+    double* r = arena<double>(ctx, 1);
+    launch_weighted_loglik(ctx, md, px, pw, n, r);
+    *out = read_scalar(ctx, r);
+  });
+}
+
+int vdfcg_pdf_divergences(vdfcg_ctx* ctx, const double* p, const double* q, int64_t n,
+                          double area, double* jsd, double* kl_pq, double* kl_qp) {
+  return guard_impl([&] {
+    begin(ctx);
+    if (n < 0 || (n > 0 && (!p || !q))) throw InvalidArgument("null grid");
+    const double* dp = stage_in(ctx, p, size_t(n)).dev;
+    const double* dq = stage_in(ctx, q, size_t(n)).dev;
+    double* r = arena<double>(ctx, 3);
+    launch_pdf_divergences(ctx, dp, dq, n, area, r);
+    double h[3];
+    VDFCG_CUDA(cudaMemcpyAsync(h, r, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    if (kl_pq) *kl_pq = h[1];
+    if (kl_qp) *kl_qp = h[2];
+    if (jsd) {  // metrics.cpp:41-45
+      constexpr double ln2 = 0.6931471805599453;
+      if (h[0] < -1e-9 || h[0] > ln2 + 1e-9)
+        throw RuntimeError("jsd outside [0, ln 2] beyond numerical slack");
+      *jsd = std::min(std::max(h[0], 0.0), ln2);
+    }
   });
 }
 

@@ -72,6 +72,12 @@ class GridSpec:
     def center_y(self, j: int) -> float:
         return self.y.lo + (j + 0.5) * self.dy()
 
+    def bin_area(self) -> float:
+        return self.dx() * self.dy()
+
+    def valid(self) -> bool:
+        return self.n_bins >= 1 and self.x.valid() and self.y.valid()
+
 
 @dataclass
 class AffineMap:
