@@ -3,9 +3,9 @@
 // cell_metrics_kernel: one CTA per cell (grid-stride over cells) computes the
 // reference's MetricsReport (pipeline.cpp:106-128) from the cell's compacted histogram
 // and fitted model:
-//   * model pdf on the full bins^d grid (evaluate_pdf, wgmm.cpp:425-453): one row of the
-//     innermost axis per thread, so the (d-1) leading terms of the triangular solve are
-//     hoisted out of the row loop; reduced to  sum q  and  #(q > 0);
+//   * model pdf on the full bins^d grid (evaluate_pdf, wgmm.cpp:425-453), reduced to
+//     sum q (an exp-free recurrence along each innermost-axis row, see below) and
+//     #(q > 0) (exact underflow intervals per row);
 //   * a pass over the non-empty bins for kl_pq / kl_qp / jsd (metrics.cpp:12-46; bins
 //     with p = 0 contribute  0.5 qn ln 2  to the JSD and make kl_qp divergent, so they
 //     need only the full-grid sums), weighted_loglik (wgmm.cpp:257-267), the data
@@ -72,6 +72,37 @@ VDFCG_DEV double log_gauss(const PrepComp& p, const double* x) {
   return -0.5 * (p.cst + q);
 }
 
+// x < this => exp(x) rounds to 0 (half the smallest subnormal, 2^-1075)
+constexpr double kExpUnderflow = -745.1332191019411;
+
+// Bin centres of the leading (d-1) axes of innermost-axis row `row`.
+template <int D>
+VDFCG_DEV void lead_coords(int64_t row, int nb, const double* lo, const double* dx, double* x) {
+#pragma unroll
+  for (int a = D - 2; a >= 0; --a) {
+    const int i = static_cast<int>(row % nb);
+    row /= nb;
+    x[a] = __dadd_rn(lo[a], __dmul_rn(static_cast<double>(i) + 0.5, dx[a]));
+  }
+}
+
+// Row-invariant part of the triangular solve: y_last = (x_last + base) * lin and the
+// squared leading terms q0.
+template <int D>
+VDFCG_DEV void row_terms(const PrepComp& p, const double* x, double& base, double& lin, double& q0) {
+  const double y0 = (x[0] - p.mu[0]) * p.L[3];
+  if (D == 2) {
+    base = -p.mu[1] - p.L[0] * y0;
+    lin = p.L[4];
+    q0 = y0 * y0;
+  } else {
+    const double y1 = (x[1] - p.mu[1] - p.L[0] * y0) * p.L[4];
+    base = -p.mu[2] - p.L[1] * y0 - p.L[2] * y1;
+    lin = p.L[5];
+    q0 = y0 * y0 + y1 * y1;
+  }
+}
+
 // Fixed-order block reduction of NV sums; every thread gets the totals in `v`.
 template <int NV>
 VDFCG_DEV void block_sum(double (&v)[NV], double* red) {
@@ -114,11 +145,6 @@ __global__ void __launch_bounds__(kMB) cell_metrics_kernel(CellsDev c, CellBinsD
     total_bins *= nb;
   }
   const int64_t rows = total_bins / nb;
-  // innermost-axis rows split into `segs` segments so 2V grids (few rows) fill the CTA
-  int64_t sg = (4 * kMB + rows - 1) / rows;
-  sg = sg < 1 ? 1 : (sg > nb ? nb : sg);
-  const int segs = static_cast<int>(sg);
-  const int seg_len = (nb + segs - 1) / segs;
   for (int cell = blockIdx.x; cell < c.n_cells; cell += gridDim.x) {
     const int M = r.comps[cell];
     const double in_range = b.in_range[cell];
@@ -150,45 +176,92 @@ __global__ void __launch_bounds__(kMB) cell_metrics_kernel(CellsDev c, CellBinsD
       __syncthreads();
       continue;
     }
-    // ---- full grid: sum q and #(q > 0), one innermost-axis row per thread
+    // ---- full grid: sum q and #(q > 0)
     double g[2] = {0.0, 0.0};
-    for (int64_t item = threadIdx.x; item < rows * segs; item += kMB) {
-      const int64_t row = item / segs;
-      const int j0 = static_cast<int>(item % segs) * seg_len, j1 = min(nb, j0 + seg_len);
+    const double dxl = dx[D - 1], lol = lo[D - 1];
+    // (a) sum q over (row, component) items. Along the innermost axis the exponent is
+    // quadratic in j, so exp(E(j+1)) = exp(E(j)) * g_j with g_{j+1} = g_j * h and
+    // h = exp(-delta^2), delta = dx / L_dd: two multiplies per bin instead of an exp.
+    // Each row walks out from the component's peak in both directions (values fall
+    // monotonically, so nothing overflows), re-anchoring with a direct exp every 32
+    // bins (relative error ~32^2 eps); a direction stops once its anchor underflows.
+    for (int64_t item = threadIdx.x; item < rows * M; item += kMB) {
+      const int64_t row = item / M;
+      const int k = static_cast<int>(item % M);
       double x[3];
-      int64_t rr = row;
-#pragma unroll
-      for (int a = D - 2; a >= 0; --a) {
-        const int i = static_cast<int>(rr % nb);
-        rr /= nb;
-        x[a] = __dadd_rn(lo[a], __dmul_rn(static_cast<double>(i) + 0.5, dx[a]));
+      lead_coords<D>(row, nb, lo, dx, x);
+      double base, lin, q0;
+      row_terms<D>(comp[k], x, base, lin, q0);
+      const double w = comp[k].w, c0 = comp[k].cst + q0;
+      const double delta = dxl * lin, hh = exp(-delta * delta), half = 0.5 * delta * delta;
+      const double yfirst = (__dadd_rn(lol, __dmul_rn(0.5, dxl)) + base) * lin;
+      const int js = static_cast<int>(fmin(fmax(rint(-yfirst / delta), 0.0), double(nb - 1)));
+      double sq = 0.0;
+      for (int j = js; j < nb; j += 32) {
+        const double y = (__dadd_rn(lol, __dmul_rn(static_cast<double>(j) + 0.5, dxl)) + base) * lin;
+        double v = w * exp(-0.5 * (c0 + y * y));
+        if (!(v > 0.0)) break;
+        double gg = exp(-(y * delta + half));
+        const int e = min(nb, j + 32);
+        for (int t = j; t < e; ++t) {
+          sq += v;
+          v *= gg;
+          gg *= hh;
+        }
       }
-      // per component: the row-invariant part of the solve
-      double base[kMaxK], lin[kMaxK], q0[kMaxK];
+      for (int j = js - 1; j >= 0; j -= 32) {
+        const double y = (__dadd_rn(lol, __dmul_rn(static_cast<double>(j) + 0.5, dxl)) + base) * lin;
+        double v = w * exp(-0.5 * (c0 + y * y));
+        if (!(v > 0.0)) break;
+        double bb = exp(y * delta - half);
+        const int e = max(-1, j - 32);
+        for (int t = j; t > e; --t) {
+          sq += v;
+          v *= bb;
+          bb *= hh;
+        }
+      }
+      g[0] += sq;
+    }
+    // (b) #(q > 0): bin j of a row has q > 0 iff some component's log term
+    // log w - (c0 + y_j^2)/2 is above the exp underflow limit — the union over the
+    // components of one interval of j each.
+    for (int64_t row = threadIdx.x; row < rows; row += kMB) {
+      double x[3];
+      lead_coords<D>(row, nb, lo, dx, x);
+      int ia[kMaxK], ib[kMaxK];
+      int ni = 0;
       for (int k = 0; k < M; ++k) {
-        const PrepComp& p = comp[k];
-        const double y0 = (x[0] - p.mu[0]) * p.L[3];
-        if (D == 2) {
-          base[k] = -p.mu[1] - p.L[0] * y0;
-          lin[k] = p.L[4];
-          q0[k] = y0 * y0;
+        double base, lin, q0;
+        row_terms<D>(comp[k], x, base, lin, q0);
+        const double R = 2.0 * (comp[k].logw - kExpUnderflow) - comp[k].cst - q0;
+        if (!(R > 0.0)) continue;
+        const double rt = sqrt(R), delta = dxl * lin;
+        const double yfirst = (__dadd_rn(lol, __dmul_rn(0.5, dxl)) + base) * lin;
+        const double a = fmax(ceil((-rt - yfirst) / delta), 0.0);
+        const double b2 = fmin(floor((rt - yfirst) / delta), double(nb - 1));
+        if (!(a <= b2)) continue;
+        int p = ni++;
+        while (p > 0 && ia[p - 1] > static_cast<int>(a)) {  // insertion sort by start
+          ia[p] = ia[p - 1];
+          ib[p] = ib[p - 1];
+          --p;
+        }
+        ia[p] = static_cast<int>(a);
+        ib[p] = static_cast<int>(b2);
+      }
+      int cnt = 0, cur_a = -1, cur_b = -2;
+      for (int t = 0; t < ni; ++t) {
+        if (ia[t] > cur_b + 1) {
+          cnt += cur_b - cur_a + 1;
+          cur_a = ia[t];
+          cur_b = ib[t];
         } else {
-          const double y1 = (x[1] - p.mu[1] - p.L[0] * y0) * p.L[4];
-          base[k] = -p.mu[2] - p.L[1] * y0 - p.L[2] * y1;
-          lin[k] = p.L[5];
-          q0[k] = y0 * y0 + y1 * y1;
+          cur_b = max(cur_b, ib[t]);
         }
       }
-      for (int j = j0; j < j1; ++j) {
-        const double xl = __dadd_rn(lo[D - 1], __dmul_rn(static_cast<double>(j) + 0.5, dx[D - 1]));
-        double q = 0.0;
-        for (int k = 0; k < M; ++k) {
-          const double y = (xl + base[k]) * lin[k];
-          q += comp[k].w * exp(-0.5 * (comp[k].cst + (q0[k] + y * y)));
-        }
-        g[0] += q;
-        g[1] += q > 0.0 ? 1.0 : 0.0;
-      }
+      cnt += cur_b - cur_a + 1;
+      g[1] += static_cast<double>(cnt);
     }
     block_sum<2>(g, red);
     const double sum_q = g[0], n_qpos = g[1];
