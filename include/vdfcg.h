@@ -280,6 +280,34 @@ int vdfcg_pack_cells(vdfcg_ctx* ctx, int32_t n_cells, int32_t dimension,
                      const vdfcg_cell_results* res, const vdfcg_model_meta* meta,
                      uint8_t* records, int64_t capacity, int64_t* record_offsets);
 
+/* ---- Record streams ----------------------------------------
+ * A stream file is a plain concatenation of standard FORMATS.md payloads — .gmmc
+ * records (kind 0) or .h2d histogram payloads (kind 1, n_bins^2 f64, x bin = row) — so
+ * every record stays decodable by the reference's decode_model / decode_histogram.
+ * `<path>.idx` indexes it: "GMIX", u8 version (1), u8 kind, u16 reserved, u64 count, then
+ * per record {i64 cell, u64 offset, u32 length, u32 crc32 (zlib) of the record bytes,
+ * f64 aux (h2d: out_of_range_count; gmmc: 0)}, little-endian. Cells whose fit failed
+ * have length 0. Appends copy device data to pinned staging on the context stream and
+ * return; a per-stream IO thread waits for each copy and writes it, so file IO
+ * overlaps the next batch's kernels. A stream is used by one host thread at a time. */
+typedef struct vdfcg_stream vdfcg_stream;
+
+#define VDFCG_STREAM_GMMC 0
+#define VDFCG_STREAM_H2D 1
+
+int vdfcg_stream_open(const char* path, int32_t kind, vdfcg_stream** out);
+/* Records of cells [cell_base, cell_base + n_cells) as produced by vdfcg_pack_cells /
+ * vdfcg_compress_cells (host or device buffers). */
+int vdfcg_stream_append_records(vdfcg_stream* s, vdfcg_ctx* ctx, const uint8_t* records,
+                                const int64_t* record_offsets, int32_t n_cells,
+                                int64_t cell_base);
+/* One .h2d payload per 2V cell (encode_histogram, codec.cpp:260-267) from compacted
+ * cell histograms (vdfcg_bin_cells output; host or device). */
+int vdfcg_stream_append_h2d(vdfcg_stream* s, vdfcg_ctx* ctx, const vdfcg_cells* cells,
+                            const vdfcg_cell_bins* bins, int64_t cell_base);
+/* Wait for every pending write, write the index, close the files. */
+int vdfcg_stream_close(vdfcg_stream* s, int64_t* n_records, int64_t* n_bytes);
+
 /* ---- Fit quality ------------------------------------------- */
 
 /* Per-cell MetricsReport (metrics.hpp:39-54) as assemble_metrics computes it

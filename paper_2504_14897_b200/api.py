@@ -220,5 +220,8 @@ def validate_fit_config(config: FitConfig, d: int) -> None:
     _marshal.check(lib().vdfcg_validate_fit_config(C.byref(cfg), d), last_error)
 
 
+from .codec import (DecodedModel, decode_histogram, decode_model,  # noqa: E402,F401
+                    encode_histogram, histogram_sidecar)
+from .stream import RecordStream, read_index, read_record  # noqa: E402,F401
 from .cells import (CellBatch, CellMetrics, bin_cells, cell_metrics,  # noqa: E402,F401
                     compress_cells, fit_cells, pack_cells, synth_cells)
