@@ -652,6 +652,163 @@ __global__ void __launch_bounds__(BLOCK) cells_bitmap_kernel(
   }
 }
 
+// K3c: K3b with the particle loads moved to the Tensor Memory Accelerator. Phase 1 of
+// cell c reads u/v/w from shared memory; right after it, one thread issues three 1-D
+// bulk copies (cp.async.bulk, completion counted on an mbarrier) of the NEXT cell's axis
+// slices into the same buffer, so the HBM reads of cell c+grid overlap the rank / count
+// / emit phases of cell c and no warp waits on global-load latency. Slices are widened
+// to 16-byte boundaries (bulk-copy granularity); `skew` locates the cell inside them.
+VDFCG_DEV uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+VDFCG_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+VDFCG_DEV void bar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+VDFCG_DEV void bar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Stage cell c's axis slices. The 16-byte widening never reads past element lim-1
+// (lim = offsets[n_cells]): an odd last element is loaded by this thread directly.
+template <int D>
+VDFCG_DEV void issue_cell_copy(const VelPtrs& vp, const int64_t* offsets, int c, int64_t lim,
+                               double* pbuf, int capp, uint64_t* bar) {
+  const int64_t b = offsets[c], e = offsets[c + 1];
+  const int64_t b0 = b & ~int64_t(1);
+  int64_t e0 = (e + 1) & ~int64_t(1);
+  const bool tail = e0 > lim;  // e == lim, odd
+  if (tail) e0 -= 2;
+  const uint32_t bytes = e0 > b0 ? static_cast<uint32_t>((e0 - b0) * 8) : 0u;
+  if (tail)
+#pragma unroll
+    for (int a = 0; a < D; ++a) pbuf[a * capp + (e0 - b0)] = __ldg(vp.v[a] + e0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  bar_expect(bar, bytes * D);
+  if (bytes)
+#pragma unroll
+    for (int a = 0; a < D; ++a) bulk_g2s(pbuf + a * capp, vp.v[a] + b0, bytes, bar);
+}
+
+template <int D, int BLOCK>
+__global__ void __launch_bounds__(BLOCK) cells_bitmap_tma_kernel(
+    VelPtrs vp, const int64_t* __restrict__ offsets, int n_cells, CellGeom g, int words, int ccap,
+    int capp, int32_t* nnz, uint32_t* __restrict__ keys_out, double* __restrict__ counts_out,
+    double* oor_out, double* in_range) {
+  using Scan = cub::BlockScan<unsigned, BLOCK>;
+  __shared__ typename Scan::TempStorage ss;
+  __shared__ unsigned s_oor;
+  __shared__ __align__(8) uint64_t bar;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* pbuf = reinterpret_cast<double*>(smem_raw);                    // [D][capp]
+  unsigned* bitmap = reinterpret_cast<unsigned*>(pbuf + D * capp);       // [words]
+  unsigned* wpre = bitmap + words;                                       // [words]
+  unsigned* cnt = wpre + words;                                          // [ccap]
+  unsigned* kbuf = cnt + ccap;                                           // [capp]
+  const int wpt = (words + BLOCK - 1) / BLOCK;
+  const int64_t lim = offsets[n_cells];
+  for (int t = threadIdx.x; t < words; t += BLOCK) bitmap[t] = 0u;
+  for (int t = threadIdx.x; t < ccap; t += BLOCK) cnt[t] = 0u;
+  if (threadIdx.x == 0) {
+    s_oor = 0u;
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (blockIdx.x < n_cells) issue_cell_copy<D>(vp, offsets, blockIdx.x, lim, pbuf, capp, &bar);
+  }
+  __syncthreads();
+  uint32_t parity = 0;
+  for (int c = blockIdx.x; c < n_cells; c += gridDim.x) {
+    const int64_t b = offsets[c];
+    const int nc = static_cast<int>(offsets[c + 1] - b);
+    const int skew = static_cast<int>(b & 1);
+    bar_wait(&bar, parity);
+    parity ^= 1u;
+    // 1. occupancy bits from the staged slices
+    unsigned oor = 0;
+    for (int li = threadIdx.x; li < nc; li += BLOCK) {
+      int64_t key = 0;
+      bool out = false;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const int bi = bin_index(pbuf[a * capp + skew + li], g.lo[a], g.hi[a], g.n_bins, g.inv[a]);
+        out |= bi < 0;
+        key = key * g.n_bins + bi;
+      }
+      if (out) {
+        ++oor;
+        kbuf[li] = 0xffffffffu;
+      } else {
+        atomicOr(bitmap + (key >> 5), 1u << (key & 31));
+        kbuf[li] = static_cast<unsigned>(key);
+      }
+    }
+    oor = warp_sum(oor);
+    if ((threadIdx.x & 31) == 0 && oor) atomicAdd(&s_oor, oor);
+    __syncthreads();
+    // the staging buffer is free: fetch the next cell while this one is ranked
+    if (threadIdx.x == 0 && c + static_cast<int>(gridDim.x) < n_cells)
+      issue_cell_copy<D>(vp, offsets, c + gridDim.x, lim, pbuf, capp, &bar);
+    // 2. ranks
+    unsigned local = 0;
+    for (int k = 0; k < wpt; ++k) {
+      const int wi = threadIdx.x * wpt + k;
+      if (wi < words) local += __popc(bitmap[wi]);
+    }
+    unsigned pre, total;
+    Scan(ss).ExclusiveSum(local, pre, total);
+    for (int k = 0; k < wpt; ++k) {
+      const int wi = threadIdx.x * wpt + k;
+      if (wi < words) {
+        wpre[wi] = pre;
+        pre += __popc(bitmap[wi]);
+      }
+    }
+    __syncthreads();
+    // 3. counts per rank, keys at their rank
+    for (int li = threadIdx.x; li < nc; li += BLOCK) {
+      const unsigned key = kbuf[li];
+      if (key != 0xffffffffu) {
+        const unsigned wd = key >> 5, bit = key & 31;
+        const unsigned r = wpre[wd] + __popc(bitmap[wd] & ((1u << bit) - 1u));
+        atomicAdd(cnt + r, 1u);
+        keys_out[b + r] = key;
+      }
+    }
+    __syncthreads();
+    // 4. emit counts, re-zero
+    for (unsigned r = threadIdx.x; r < total; r += BLOCK) {
+      counts_out[b + r] = static_cast<double>(cnt[r]);
+      cnt[r] = 0u;
+    }
+    for (int t = threadIdx.x; t < words; t += BLOCK) bitmap[t] = 0u;
+    if (threadIdx.x == 0) {
+      const unsigned to = s_oor;
+      nnz[c] = static_cast<int32_t>(total);
+      oor_out[c] = static_cast<double>(to);
+      in_range[c] = static_cast<double>(nc - static_cast<int>(to));
+      s_oor = 0u;
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void chunks_per_cell_kernel(const int64_t* offsets, int n_cells, int64_t chunk,
                                        int64_t* out) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n_cells; c += gridDim.x * blockDim.x) {
@@ -761,7 +918,31 @@ static void bin_cells_d(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
   const int64_t words = (bins + 31) / 32;
   const int64_t ccap = std::max<int64_t>(1, std::min<int64_t>(maxc, bins));  // >= every nnz
   const int64_t kcap = std::min<int64_t>(maxc, 4096);
-  if (!weighted && sparse && words * 8 + ccap * 4 + kcap * 4 <= 160 * 1024) {
+  // TMA-staged variant: every axis base 16-byte aligned and the staging buffer (largest
+  // cell + 16-byte slack per axis) fits beside the bitmap with two CTAs per SM.
+  const int64_t capp = ((maxc + 2 + 1) / 2) * 2;
+  const size_t tma_smem = size_t(D) * capp * 8 + size_t(words) * 8 + size_t(ccap) * 4 + size_t(capp) * 4;
+  bool aligned = true;
+  for (int a = 0; a < D; ++a) aligned = aligned && (reinterpret_cast<uintptr_t>(c.vel[a]) & 15) == 0;
+  static const int tma_env = [] {
+    const char* e = getenv("VDFCG_HIST_TMA");  // 0: off, 1: 512-thread CTAs, 2: 256
+    return e ? atoi(e) : 1;
+  }();
+  const int tb = tma_env == 2 ? 256 : 512;
+  if (!weighted && sparse && aligned && tma_env && tma_smem <= 110 * 1024) {
+    auto k = tb == 512 ? cells_bitmap_tma_kernel<D, 512> : cells_bitmap_tma_kernel<D, 256>;
+    VDFCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tma_smem)));
+    int occ = 0;
+    VDFCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, tb, tma_smem));
+    const int grid = std::max(1, std::min(c.n_cells, ctx->sm_count * std::max(occ, 1)));
+    VelPtrs vp{{c.vel[0], c.vel[1], c.vel[2]}};
+    VDFCG_LAUNCH(ctx, "cells_bitmap_tma",
+                 k<<<grid, tb, tma_smem, ctx->stream>>>(vp, c.offsets, c.n_cells, g, static_cast<int>(words),
+                                                        static_cast<int>(ccap), static_cast<int>(capp),
+                                                        out.nnz, out.keys, out.counts, out.oor, out.in_range));
+    done = true;
+  }
+  if (!done && !weighted && sparse && words * 8 + ccap * 4 + kcap * 4 <= 160 * 1024) {
     const int cap = static_cast<int>(std::max<int64_t>(kcap, 1));
     const size_t smem = size_t(words) * 8 + size_t(ccap) * 4 + size_t(cap) * 4;
     auto k = cells_bitmap_kernel<D, 256>;

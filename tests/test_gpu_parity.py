@@ -138,7 +138,7 @@ def _cells_case(d, n_cells, per_cell, n_bins, seed=1, weighted=False):
 
 @pytest.mark.parametrize("d,n_cells,per_cell,n_bins,weighted", [
     (3, 16, 3000, 32, False),    # dense shared-memory path
-    (3, 64, 1900, 48, False),    # sparse sort path (cfg4 shape)
+    (3, 64, 1900, 48, False),    # sparse bitmap path, TMA-staged (cfg4 shape)
     (3, 32, 1900, 48, True),     # weighted: sort path, bit-exact sequential sums
     (2, 8, 50000, 64, False),    # 2V dense
     (3, 4, 20000, 64, False),    # dense global path
@@ -188,3 +188,36 @@ def test_compress_cells_parity(d, n_cells, per_cell, n_bins, K):
                  for i in range(orr.components[c])]
         mo = GmmModel(comps, AffineMap.identity(d), d)
         assert model_close(mg, mo) <= TOL_EM, c
+
+
+@pytest.mark.parametrize("misaligned", [False, True])
+def test_bin_cells_staging_edges(misaligned):
+    """Odd cell boundaries, empty first/last cells and an odd particle total exercise the
+    16-byte widening of the TMA-staged bitmap kernel; 8-byte-misaligned device axes take
+    the non-TMA bitmap kernel. Both must equal the oracle bit for bit."""
+    import torch
+    rng = np.random.default_rng(21)
+    counts = rng.integers(1, 2400, size=97)
+    counts[[0, 5, 96]] = 0
+    counts[1] = 1
+    if counts.sum() % 2 == 0:
+        counts[2] += 1
+    offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    n = int(offs[-1])
+    v = np.asfortranarray(rng.normal(size=(n, 3)) * 1.7)
+    ob = O.bin_cells(O.CellsHost(v, offs, 48, [-6] * 3, [6] * 3))
+    dev = torch.device("cuda", 0)
+    if misaligned:
+        axes = [torch.from_numpy(np.concatenate([[0.0], v[:, a]])).to(dev)[1:] for a in range(3)]
+        assert axes[0].data_ptr() % 16 == 8
+    else:
+        axes = [torch.from_numpy(np.ascontiguousarray(v[:, a])).to(dev) for a in range(3)]
+    gb = G.bin_cells(G.CellBatch(axes, torch.from_numpy(offs).to(dev), 48, [-6] * 3, [6] * 3))
+    nnz = gb.nnz.cpu().numpy()
+    keys, cnts = gb.keys.cpu().numpy(), gb.counts.cpu().numpy()
+    assert np.array_equal(nnz, ob.nnz)
+    for c in range(len(counts)):
+        b, k = offs[c], ob.nnz[c]
+        assert np.array_equal(keys[b:b + k], ob.keys[b:b + k])
+        assert np.array_equal(cnts[b:b + k], ob.counts[b:b + k])
+    assert np.array_equal(gb.out_of_range.cpu().numpy(), ob.out_of_range)
