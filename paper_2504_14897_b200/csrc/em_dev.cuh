@@ -188,6 +188,40 @@ VDFCG_DEV double exp_nonpos(double x, const double* tab) {
   return __hiloint2double(__double2hiint(v) + ((k >> SH) << 20), __double2loint(v));
 }
 
+// Log2-domain E-step (VDFCG_LOG2=1, default): the affine form is pre-scaled by
+// sqrt(log2(e)/2) and cst by log2(e), so a component's term is
+//   lp2 = cst2 - |A2 z - b2|^2 = log2(e) * (cst - |A z - b|^2 / 2)
+// (three FMAs from cst, no separate -0.5 scaling) and 2^x needs no ln2 multiply: the
+// table index comes straight from x * 256 and the reduced argument x - k/256 is exact, so
+// the two-constant Cody-Waite step collapses to one FMA. e^(r ln 2) by a degree-4 Taylor
+// polynomial in r (|r| <= 1/512: truncation < 4e-17).
+#ifndef VDFCG_LOG2
+#define VDFCG_LOG2 1
+#endif
+__device__ __constant__ double kExp2C[7] = {
+    256.0, 6755399441055744.0, 0.00390625,
+    0.0096181291076284772,   // ln2^4 / 24
+    0.055504108664821579,    // ln2^3 / 6
+    0.24022650695910071,     // ln2^2 / 2
+    0.69314718055994531};    // ln2
+constexpr double kLog2E = 1.4426950408889634;
+constexpr double kSqrtHalfLog2E = 0.84932180028801907;  // sqrt(log2(e) / 2)
+
+// 2^x for x <= 0 (x clamped at -1021: 2^-1021 ~ 4.5e-308, below every tolerance).
+VDFCG_DEV double exp2_nonpos(double x, const double* tab) {
+  x = x < -1021.0 ? -1021.0 : x;
+  const double tm = fma(x, kExp2C[0], kExp2C[1]);
+  const int k = __double2loint(tm);
+  const double kd = tm - kExp2C[1];
+  const double r = fma(-kd, kExp2C[2], x);  // exact
+  double p = fma(r, kExp2C[3], kExp2C[4]);
+  p = fma(p, r, kExp2C[5]);
+  p = fma(p, r, kExp2C[6]);
+  p = fma(p, r, 1.0);
+  const double v = tab[k & 255] * p;
+  return __hiloint2double(__double2hiint(v) + ((k >> 8) << 20), __double2loint(v));
+}
+
 // log(s) for the per-point mixture normaliser (any positive normal double; s >= 1e-300
 // on the fast path). s = m 2^e, m in [1,2); j = top 7 mantissa bits; r = m c_j - 1 with
 // c_j ~ 1/(1 + (j+0.5)/128) so |r| < 1/256; log s = e ln2 + (-log c_j) + log1p(r) with a
@@ -313,6 +347,22 @@ VDFCG_DEV void affine_from_chol(const double* mu, const double* Lo, const double
   b[0] = a00 * mu[0];
   b[1] = D >= 2 ? a10 * mu[0] + a11 * mu[1] : 0.0;
   b[2] = D >= 3 ? a20 * mu[0] + a21 * mu[1] + a22 * mu[2] : 0.0;
+}
+
+// log2-domain term with the pre-scaled affine form (see exp2_nonpos).
+template <int D>
+VDFCG_DEV double comp_logp2_affine(const double* z, const double* A, const double* b, double cst) {
+  const double y0 = fma(A[0], z[0], -b[0]);
+  double lp = fma(-y0, y0, cst);
+  if (D >= 2) {
+    const double y1 = fma(A[2], z[1], fma(A[1], z[0], -b[1]));
+    lp = fma(-y1, y1, lp);
+  }
+  if (D >= 3) {
+    const double y2 = fma(A[5], z[2], fma(A[4], z[1], fma(A[3], z[0], -b[2])));
+    lp = fma(-y2, y2, lp);
+  }
+  return lp;
 }
 
 template <int D>

@@ -145,7 +145,11 @@ VDFCG_DEV void em_pass(const Src& src, int n, EmState<D, K>& S, double* red) {
 #pragma unroll
     for (int j = 0; j < KL; ++j) {
       const int i = slot0 + j;
+#if VDFCG_LOG2
+      lp[j] = comp_logp2_affine<D>(z, S.A[i], S.bv[i], S.cst[i]);
+#else
       lp[j] = comp_logp_affine<D>(z, S.A[i], S.bv[i], S.cst[i]);
+#endif
       mx = lp[j] > mx ? lp[j] : mx;
     }
 #pragma unroll
@@ -156,12 +160,20 @@ VDFCG_DEV void em_pass(const Src& src, int n, EmState<D, K>& S, double* red) {
     double sum = 0.0;
 #pragma unroll
     for (int j = 0; j < KL; ++j) {
+#if VDFCG_LOG2
+      lp[j] = exp2_nonpos(lp[j] - mx, S.exp2tab);
+#else
       lp[j] = exp_nonpos(lp[j] - mx, S.exp2tab);
+#endif
       sum += lp[j];
     }
 #pragma unroll
     for (int o = 1; o < SP; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+#if VDFCG_LOG2
+    if (!EXACT && part == 0) ll += w * fma(mx, 0.6931471805599453, log_ge1(sum, S.logtab));
+#else
     if (!EXACT && part == 0) ll += w * (mx + log_ge1(sum, S.logtab));
+#endif
     const double ws = w * rcp_newton(sum);
     if (!EXACT) {
       // Pass 1 accumulates about the frame origin (z is the normalised coordinate,
@@ -282,16 +294,28 @@ VDFCG_DEV void em_pass_f32(const Src& src, int n, EmState<D, K>& S, double* red)
         const float y2 = fmaf(S.Af[i][5], zf[2], fmaf(S.Af[i][4], zf[1], fmaf(S.Af[i][3], zf[0], -S.bf[i][2])));
         q = fmaf(y2, y2, q);
       }
+#if VDFCG_LOG2
+      u[i] = S.cstf[i] - q;  // log2 domain (pre-scaled affine form)
+#else
       u[i] = fmaf(-0.5f, q, S.cstf[i]);
+#endif
       mx = u[i] > mx ? u[i] : mx;
     }
     float sum = 0.0f;
 #pragma unroll
     for (int i = 0; i < KP; ++i) {
+#if VDFCG_LOG2
+      u[i] = ex2f_approx(u[i] - mx);
+#else
       u[i] = ex2f_approx((u[i] - mx) * 1.4426950408889634f);
+#endif
       sum += u[i];
     }
+#if VDFCG_LOG2
+    ll += w * (0.6931471805599453 * (static_cast<double>(mx) + static_cast<double>(lg2f_approx(sum))));
+#else
     ll += w * (static_cast<double>(mx) + 0.6931471805599453 * static_cast<double>(lg2f_approx(sum)));
+#endif
     const float inv = __frcp_rn(sum);
     double zz[D * (D + 1) / 2];
 #pragma unroll
@@ -386,6 +410,13 @@ VDFCG_DEV void run_fit(const Src& src, int n, EmState<D, K>& S, double* red, con
       if (lane < S.m) {
         dead = !prep_component<D>(S.cov[lane], S.alpha[lane], S.Lo[lane], S.rd[lane], &S.cst[lane]);
         affine_from_chol<D>(S.mu[lane], S.Lo[lane], S.rd[lane], S.A[lane], S.bv[lane]);
+#if VDFCG_LOG2
+#pragma unroll
+        for (int e = 0; e < 6; ++e) S.A[lane][e] *= kSqrtHalfLog2E;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) S.bv[lane][a] *= kSqrtHalfLog2E;
+        S.cst[lane] *= kLog2E;
+#endif
 #pragma unroll
         for (int a = 0; a < D; ++a) S.muc[lane][a] = S.mu[lane][a];
 #pragma unroll
@@ -603,6 +634,17 @@ VDFCG_DEV void run_fit(const Src& src, int n, EmState<D, K>& S, double* red, con
 #pragma unroll
         for (int b = 0; b < D; ++b) out.cov[((base + i) * D + a) * D + b] = cv(a, b);
       }
+    }
+  }
+  // slots past the fitted components (and every slot of a failed cell) are zeroed, so
+  // result buffers are fully defined and bitwise reproducible
+  for (int i = (S.status == 0 ? S.m : 0) + threadIdx.x; i < K_out; i += blockDim.x) {
+    out.w[base + i] = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      out.mu[(base + i) * D + a] = 0.0;
+#pragma unroll
+      for (int b = 0; b < D; ++b) out.cov[((base + i) * D + a) * D + b] = 0.0;
     }
   }
   if (threadIdx.x == 0) {
