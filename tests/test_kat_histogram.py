@@ -70,10 +70,13 @@ def test_all_planes_d2_rejected_and_empty_degenerate(impl):  # :119-134
         assert h.degenerate() and not h.counts.any()
 
 
-def test_all_planes_maxwellian_marginals_mass(impl):  # :106-117 (mass part; JSD is metrics)
-    p = O.preset("maxwellian", 200000, 5)
-    for h in impl.all_planes(p, 200, AxisRange(-5, 5)):
-        assert abs(h.in_range_count() + h.out_of_range_count - 2e5) <= 1e-9 * 2e5
+def test_all_planes_maxwellian_marginals_mass(impl):  # :106-117
+    p = O.preset("maxwellian", 1000000, 5)
+    hs = impl.all_planes(p, 200, AxisRange(-5, 5))
+    for h in hs:
+        assert abs(h.in_range_count() + h.out_of_range_count - 1e6) <= 1e-9 * 1e6
+    a, b, c = (impl.to_pdf(h) for h in hs)
+    assert impl.jsd(a, b) < 0.01 and impl.jsd(b, c) < 0.01 and impl.jsd(a, c) < 0.01
 
 
 def test_to_weighted_points_order_centres_total(impl):  # :136-156
