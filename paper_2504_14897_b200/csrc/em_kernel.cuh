@@ -217,6 +217,21 @@ VDFCG_DEV void em_pass(const Src& src, int n, EmState<D, K>& S, double* red) {
   }
   // fixed-order reduction: lanes of the same part (xor tree) -> warps (ascending)
   constexpr int W = K * NS + 1;
+  if (SP == 1) {  // reduce-scatter: each lane ends with ~2 of the K*NS+1 warp totals
+    double v[KL * NS + 1];
+#pragma unroll
+    for (int j = 0; j < KL; ++j)
+#pragma unroll
+      for (int t = 0; t < NS; ++t) v[j * NS + t] = acc[j][t];
+    v[KL * NS] = EXACT ? 0.0 : ll;
+    int start, count;
+    warp_scatter_sum(v, lane, start, count);
+#pragma unroll
+    for (int j = 0; j < WarpScatter<KL * NS + 1>::HOUT; ++j) {
+      const int gi = start + j;
+      if (j < count && (gi == K * NS ? !EXACT : gi / NS < m)) red[warp * W + gi] = v[j];
+    }
+  } else {
 #pragma unroll
   for (int j = 0; j < KL; ++j) {
 #pragma unroll
@@ -231,6 +246,7 @@ VDFCG_DEV void em_pass(const Src& src, int n, EmState<D, K>& S, double* red) {
   if (!EXACT) {
     const double v = warp_sum(ll);
     if (lane == 0) red[warp * W + K * NS] = v;
+  }
   }
   __syncthreads();
   for (int t = threadIdx.x; t < W; t += blockDim.x) {
