@@ -1,6 +1,7 @@
 """Readers for the FORMATS.md payloads the device path writes (codec.hpp:50-64).
 
-``decode_model`` (codec.cpp:136-190) and the ``.h2d`` helpers (codec.cpp:260-300) are
+``decode_model`` (codec.cpp:136-190), the ``.gmm.json`` rendering (codec.cpp:192-255) and
+the ``.h2d`` helpers (codec.cpp:260-300) are
 byte-format parsing on the host — the reference does the same on the host — used to
 read back ``.gmmc`` records and record streams. Errors raise ``CodecError`` with the
 reference's messages.
@@ -15,7 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .types import (AffineMap, AxisRange, CodecError, GaussianComponent, GmmModel, Histogram2D,
-                    ModelMeta, Plane)
+                    InvalidArgument, ModelMeta, Plane)
 
 _PLANES = {0: Plane.uv, 1: Plane.vw, 2: Plane.uw}
 _PLANE_NAMES = {Plane.uv: "uv", Plane.vw: "vw", Plane.uw: "uw"}
@@ -105,6 +106,54 @@ def decode_model(data: bytes) -> DecodedModel:
         comps.append(GaussianComponent(w, mean, cov))
     return DecodedModel(GmmModel(comps, AffineMap.identity(d), d),
                         ModelMeta(label, plane, cycle, ranges))
+
+
+def model_to_json(model: GmmModel, meta: ModelMeta) -> dict:
+    """codec.cpp:192-220 (`.gmm.json`): same information as `.gmmc`; json.dumps prints
+    doubles in their shortest round-trip form, so parsing reproduces the exact bits.
+    Expects a canonical (data-space) model, as the writers produce."""
+    model.validate()
+    if not model.normalization.is_identity():
+        raise InvalidArgument("model_to_json: denormalize the model first (denormalize_model)")
+    d = model.dimension
+    if len(meta.axis_ranges) != d:
+        raise InvalidArgument("model meta must carry one axis range per dimension")
+    comps = []
+    for c in model.components:
+        cov = np.asarray(c.covariance, float)
+        comps.append({"weight": float(c.weight), "mean": [float(x) for x in c.mean],
+                      "covariance_upper": [float(cov[i, j]) for i in range(d) for j in range(i, d)]})
+    return {"format": "gmm-model", "version": 1, "dimension": d, "components": comps,
+            "plane": _PLANE_NAMES[Plane(meta.plane)] if meta.plane is not None else None,
+            "species": meta.species_label, "cycle": int(meta.cycle),
+            "axis_ranges": [[r.lo, r.hi] for r in meta.axis_ranges]}
+
+
+def model_from_json(j) -> DecodedModel:
+    """codec.cpp:222-255."""
+    if isinstance(j, (str, bytes)):
+        j = json.loads(j)
+    if j.get("format", "") != "gmm-model":
+        raise CodecError("not a gmm-model JSON document")
+    if j["version"] != 1:
+        raise CodecError("unsupported gmm-model JSON version")
+    d = int(j["dimension"])
+    iu = np.triu_indices(d)
+    comps = []
+    for jc in j["components"]:
+        mean, upper = jc["mean"], jc["covariance_upper"]
+        if len(mean) != d or len(upper) != d * (d + 1) // 2:
+            raise CodecError("component shape mismatch")
+        cov = np.zeros((d, d))
+        cov[iu] = upper
+        cov[(iu[1], iu[0])] = cov[iu]
+        if not _llt_ok(cov):
+            raise CodecError("decoded covariance is not symmetric positive definite")
+        comps.append(GaussianComponent(float(jc["weight"]), np.array(mean, float), cov))
+    names = {v: k for k, v in _PLANE_NAMES.items()}
+    plane = None if j["plane"] is None else names[j["plane"]]
+    meta = ModelMeta(j["species"], plane, int(j["cycle"]), [AxisRange(*r) for r in j["axis_ranges"]])
+    return DecodedModel(GmmModel(comps, AffineMap.identity(d), d), meta)
 
 
 def encode_histogram(hist: Histogram2D) -> bytes:

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <exception>
 #include <functional>
 #include <string>
 #include <vector>
@@ -937,6 +938,33 @@ static void pack_into(vdfcg_ctx* ctx, const CellsDev& c, const EmOut& o,
   });
 }
 
+// Events owned for the duration of one call (destroyed on every exit path).
+struct EventPool {
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t make() {
+    cudaEvent_t e;
+    VDFCG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ev.push_back(e);
+    return e;
+  }
+  ~EventPool() {
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+};
+
+// On an exception, drain the side streams before the arena can be reused by the next call
+// (their copies / kernels may still target this call's buffers).
+struct SideStreamGuard {
+  vdfcg_ctx* ctx;
+  int pending = std::uncaught_exceptions();
+  ~SideStreamGuard() {
+    if (std::uncaught_exceptions() > pending) {
+      cudaStreamSynchronize(ctx->copy_stream);
+      cudaStreamSynchronize(ctx->aux_stream);
+    }
+  }
+};
+
 // Host-resident particles: the velocity (and weight) ranges of successive cell chunks are
 // copied on the context's copy stream while the compute stream bins and fits the chunks
 // already resident, so the end-to-end time approaches max(H2D, compute) instead of the sum.
@@ -997,11 +1025,13 @@ static bool compress_pipelined(vdfcg_ctx* ctx, const vdfcg_cells* cells,
   }
   bounds.push_back(nc);
   // the copy stream starts after everything already queued on the compute stream
-  cudaEvent_t start;
-  VDFCG_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  EventPool events;
+  SideStreamGuard side{ctx};
+  cudaEvent_t start = events.make();
   VDFCG_CUDA(cudaEventRecord(start, ctx->stream));
   VDFCG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, start, 0));
   std::vector<cudaEvent_t> ready(bounds.size() - 1);
+  for (auto& e : ready) e = events.make();
   for (size_t j = 0; j + 1 < bounds.size(); ++j) {
     const int64_t p0 = hoff[bounds[j]], p1 = hoff[bounds[j + 1]];
     const size_t bytes = size_t(p1 - p0) * sizeof(double);
@@ -1013,7 +1043,6 @@ static bool compress_pipelined(vdfcg_ctx* ctx, const vdfcg_cells* cells,
         VDFCG_CUDA(cudaMemcpyAsync(dw + p0, cells->weights + p0, bytes, cudaMemcpyHostToDevice,
                                    ctx->copy_stream));
     }
-    VDFCG_CUDA(cudaEventCreateWithFlags(&ready[j], cudaEventDisableTiming));
     VDFCG_CUDA(cudaEventRecord(ready[j], ctx->copy_stream));
   }
   validate_config(cfg, d);
@@ -1026,9 +1055,7 @@ static bool compress_pipelined(vdfcg_ctx* ctx, const vdfcg_cells* cells,
   // start while the previous chunk's last fits drain. Every fit is independent, so the
   // results do not depend on the interleaving.
   cudaStream_t main = ctx->stream;
-  cudaEvent_t fork, join;
-  VDFCG_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-  VDFCG_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+  cudaEvent_t fork = events.make(), join = events.make();
   VDFCG_CUDA(cudaEventRecord(fork, main));
   VDFCG_CUDA(cudaStreamWaitEvent(ctx->aux_stream, fork, 0));
   try {
@@ -1056,13 +1083,9 @@ static bool compress_pipelined(vdfcg_ctx* ctx, const vdfcg_cells* cells,
   ctx->stream = main;
   VDFCG_CUDA(cudaEventRecord(join, ctx->aux_stream));
   VDFCG_CUDA(cudaStreamWaitEvent(main, join, 0));
-  cudaEventDestroy(fork);
-  cudaEventDestroy(join);
   pack_into(ctx, c, o, meta, records, capacity, record_offsets, fin);
   for (auto& f : fin) f();
   sync(ctx);
-  cudaEventDestroy(start);
-  for (auto e : ready) cudaEventDestroy(e);
   return true;
 }
 

@@ -88,3 +88,23 @@ def test_empty_stream_writes_index(tmp_path):
     from paper_2504_14897_b200.types import InvalidArgument
     with pytest.raises(InvalidArgument):
         RecordStream(str(tmp_path / "x"), 7)
+
+
+def test_model_json_round_trip():  # FORMATS.md:52-70, codec.cpp:192-255
+    rng = np.random.default_rng(8)
+    a = rng.normal(size=(3, 3))
+    cov = a @ a.T + np.eye(3)
+    cov = np.triu(cov) + np.triu(cov, 1).T
+    m = GmmModel([GaussianComponent(0.3, rng.normal(size=3), cov),
+                  GaussianComponent(0.7, rng.normal(size=3), np.eye(3) * 0.1)], AffineMap.identity(3), 3)
+    meta = ModelMeta("ions", None, 9, [AxisRange(-1.5, 2.0)] * 3)
+    j = json.loads(json.dumps(codec.model_to_json(m, meta)))
+    assert j["format"] == "gmm-model" and j["plane"] is None and len(j["components"][0]["covariance_upper"]) == 6
+    back = codec.model_from_json(j)
+    for x, y in zip(back.model.components, m.components):
+        assert x.weight == y.weight and np.array_equal(x.mean, y.mean) and np.array_equal(x.covariance, y.covariance)
+    # the JSON and the binary record carry the same information
+    dm = codec.decode_model(O.encode_model(m, meta))
+    assert [c.weight for c in dm.model.components] == [c.weight for c in back.model.components]
+    with pytest.raises(CodecError, match="gmm-model"):
+        codec.model_from_json(dict(j, format="x"))
