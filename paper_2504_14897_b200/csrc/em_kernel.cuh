@@ -834,6 +834,8 @@ VDFCG_DEV int key_prologue(const KeyCells& kc, int c, const EmConfig& cfg, EmSta
 }
 
 template <int D, int K, bool KEYS, bool F32 = false>
+// 128 registers for K <= 4 measured best on cfg4 (112: 578 ms, 120: 555, 128: 538, 136: 637,
+// 152: 547 per species): 16 resident fits per SM with a few loop-invariant spills.
 __global__ void __launch_bounds__(256) __maxnreg__(K <= 4 ? 128 : 255) em_kernel(KeyCells kc, CoordArgs ca, EmConfig cfg,
                                                  EmOut out, int* counter, int red_stride) {
   extern __shared__ __align__(16) unsigned char smem_raw[];

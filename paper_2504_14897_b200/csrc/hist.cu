@@ -564,7 +564,7 @@ __global__ void __launch_bounds__(BLOCK) cells_bitmap_kernel(
     double* oor_out, double* in_range) {
   using Scan = cub::BlockScan<unsigned, BLOCK>;
   __shared__ typename Scan::TempStorage ss;
-  __shared__ unsigned s_oor, s_nnz;
+  __shared__ unsigned s_oor;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned* bitmap = reinterpret_cast<unsigned*>(smem_raw);  // [words]
   unsigned* wpre = bitmap + words;                           // [words] exclusive prefix
