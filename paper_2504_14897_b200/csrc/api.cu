@@ -1012,13 +1012,17 @@ static bool compress_pipelined(vdfcg_ctx* ctx, const vdfcg_cells* cells,
   double* dw = cells->weights ? arena<double>(ctx, size_t(n)) : nullptr;
   for (int a = 0; a < 3; ++a) c.vel[a] = a < d ? dv[a] : dv[0];
   c.w = dw;
-  // whole-cell chunks; the first two are small (1/64, then 3/64 of the particles) so
-  // compute starts early, the rest are equal
-  const int nch = std::min(16, nc);
+  // whole-cell chunks growing geometrically (x2): the first is 1/(2^n - 1) of the
+  // particles, so compute starts after a small copy, and every later copy (55 GB/s) is done
+  // before the previous chunk's compute (~22 GB/s of input consumed) ends
+  static const int pipe_chunks = [] {
+    const char* e = getenv("VDFCG_PIPE_CHUNKS");
+    return e ? std::min(20, std::max(2, atoi(e))) : 8;
+  }();
+  const int nch = std::min(pipe_chunks, nc);
   std::vector<int> bounds{0};
   for (int j = 1; j < nch; ++j) {
-    const double f = nch < 16 ? double(j) / nch
-                     : j == 1 ? 1.0 / 64 : 1.0 / 16 + (15.0 / 16) * (j - 2) / (nch - 2);
+    const double f = double((1ll << j) - 1) / double((1ll << nch) - 1);
     const int64_t target = hoff[0] + static_cast<int64_t>(double(hoff[nc] - hoff[0]) * f);
     const int cb = static_cast<int>(std::upper_bound(hoff, hoff + nc + 1, target) - hoff) - 1;
     bounds.push_back(std::max(bounds.back(), std::min(cb, nc)));
