@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(kMB) cell_metrics_kernel(CellsDev c, CellBinsD
                                                            MetricsOut o) {
   __shared__ PrepComp comp[kMaxK];
   __shared__ double red[33 * 17];
+  __shared__ double s_delta[kMaxK], s_rdelta[kMaxK], s_hh[kMaxK];
   __shared__ int s_ok;
   const int nb = c.n_bins;
   double dx[D], lo[D];
@@ -166,8 +167,15 @@ __global__ void __launch_bounds__(kMB) cell_metrics_kernel(CellsDev c, CellBinsD
     __syncthreads();
     if (ok && threadIdx.x < M) {
       const size_t ci = size_t(cell) * r.K + threadIdx.x;
-      if (!prep_comp<D>(r.w[ci], r.mu + ci * D, r.cov + ci * D * D, comp[threadIdx.x]))
+      PrepComp& pc = comp[threadIdx.x];
+      if (!prep_comp<D>(r.w[ci], r.mu + ci * D, r.cov + ci * D * D, pc)) {
         s_ok = 0;  // evaluate_pdf: "model component covariance is not SPD"
+      } else {  // innermost-axis step of y and its recurrence factor, per component
+        const double delta = dx[D - 1] * pc.L[3 + D - 1];
+        s_delta[threadIdx.x] = delta;
+        s_rdelta[threadIdx.x] = 1.0 / delta;
+        s_hh[threadIdx.x] = exp(-delta * delta);
+      }
     }
     __syncthreads();
     ok = s_ok;
@@ -193,15 +201,23 @@ __global__ void __launch_bounds__(kMB) cell_metrics_kernel(CellsDev c, CellBinsD
       double base, lin, q0;
       row_terms<D>(comp[k], x, base, lin, q0);
       const double w = comp[k].w, c0 = comp[k].cst + q0;
-      const double delta = dxl * lin, hh = exp(-delta * delta), half = 0.5 * delta * delta;
+      const double delta = s_delta[k], hh = s_hh[k], half = 0.5 * delta * delta;
       const double yfirst = (__dadd_rn(lol, __dmul_rn(0.5, dxl)) + base) * lin;
-      const int js = static_cast<int>(fmin(fmax(rint(-yfirst / delta), 0.0), double(nb - 1)));
+      const int js = static_cast<int>(fmin(fmax(rint(-yfirst * s_rdelta[k]), 0.0), double(nb - 1)));
       double sq = 0.0;
+      // forward from the peak; the first anchor also seeds the backward walk:
+      // exp(E(js-1) - E(js)) = exp(-delta^2) / g(js)
+      double vb = 0.0, bb = 0.0;
       for (int j = js; j < nb; j += 32) {
         const double y = (__dadd_rn(lol, __dmul_rn(static_cast<double>(j) + 0.5, dxl)) + base) * lin;
         double v = w * exp(-0.5 * (c0 + y * y));
         if (!(v > 0.0)) break;
         double gg = exp(-(y * delta + half));
+        if (j == js) {
+          bb = hh / gg;
+          vb = v * bb;
+          bb *= hh;
+        }
         const int e = min(nb, j + 32);
         for (int t = j; t < e; ++t) {
           sq += v;
@@ -210,15 +226,21 @@ __global__ void __launch_bounds__(kMB) cell_metrics_kernel(CellsDev c, CellBinsD
         }
       }
       for (int j = js - 1; j >= 0; j -= 32) {
-        const double y = (__dadd_rn(lol, __dmul_rn(static_cast<double>(j) + 0.5, dxl)) + base) * lin;
-        double v = w * exp(-0.5 * (c0 + y * y));
+        double v, b2;
+        if (j == js - 1) {
+          v = vb;
+          b2 = bb;
+        } else {
+          const double y = (__dadd_rn(lol, __dmul_rn(static_cast<double>(j) + 0.5, dxl)) + base) * lin;
+          v = w * exp(-0.5 * (c0 + y * y));
+          b2 = exp(y * delta - half);
+        }
         if (!(v > 0.0)) break;
-        double bb = exp(y * delta - half);
         const int e = max(-1, j - 32);
         for (int t = j; t > e; --t) {
           sq += v;
-          v *= bb;
-          bb *= hh;
+          v *= b2;
+          b2 *= hh;
         }
       }
       g[0] += sq;
@@ -236,10 +258,10 @@ __global__ void __launch_bounds__(kMB) cell_metrics_kernel(CellsDev c, CellBinsD
         row_terms<D>(comp[k], x, base, lin, q0);
         const double R = 2.0 * (comp[k].logw - kExpUnderflow) - comp[k].cst - q0;
         if (!(R > 0.0)) continue;
-        const double rt = sqrt(R), delta = dxl * lin;
+        const double rt = sqrt(R), rdelta = s_rdelta[k];
         const double yfirst = (__dadd_rn(lol, __dmul_rn(0.5, dxl)) + base) * lin;
-        const double a = fmax(ceil((-rt - yfirst) / delta), 0.0);
-        const double b2 = fmin(floor((rt - yfirst) / delta), double(nb - 1));
+        const double a = fmax(ceil((-rt - yfirst) * rdelta), 0.0);
+        const double b2 = fmin(floor((rt - yfirst) * rdelta), double(nb - 1));
         if (!(a <= b2)) continue;
         int p = ni++;
         while (p > 0 && ia[p - 1] > static_cast<int>(a)) {  // insertion sort by start
