@@ -25,3 +25,4 @@ def test_shim_runs_on_gpu(tmp_path):
     r = subprocess.run([_build(tmp_path)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "invalid_argument: fit: degenerate data: axis 0 has zero spread" in r.stdout
+    assert "cells ok=64 records=64" in r.stdout
