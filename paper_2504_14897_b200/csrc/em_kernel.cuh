@@ -3,6 +3,7 @@
 // em_d3.cu so the exact-K variants compile in parallel. See em.cu for the overview.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cub/block/block_reduce.cuh>
 
 #include <algorithm>
@@ -109,10 +110,24 @@ VDFCG_DEV constexpr int uidx(int a, int b) {  // packed upper index, a <= b
   return D == 2 ? (a == 0 ? b : 2) : (a == 0 ? b : (a == 1 ? 2 + b : 5));
 }
 
+// Thread-block cluster (single large fits): CL=true spreads one fit's points over the CTAs
+// of a cluster; every CTA runs the (identical, deterministic) protocol and the partial
+// sufficient statistics are combined through distributed shared memory.
+template <bool CL>
+VDFCG_DEV int cluster_rank() {
+  if constexpr (CL) return static_cast<int>(cooperative_groups::this_cluster().block_rank());
+  else return 0;
+}
+template <bool CL>
+VDFCG_DEV int cluster_size() {
+  if constexpr (CL) return static_cast<int>(cooperative_groups::this_cluster().num_blocks());
+  else return 1;
+}
+
 // ---------------------------------------------------------------- the point pass
 // EXACT=false: pass 1, statistics centred on mu_old (+ loglik). EXACT=true: the
 // covariance sums centred on mu_new for the components flagged in exact_mask.
-template <int D, int K, bool EXACT, class Src>
+template <int D, int K, bool EXACT, bool CL, class Src>
 VDFCG_DEV void em_pass(const Src& src, int n, EmState<D, K>& S, double* red) {
   constexpr int NS = NStat<D>::value;
   constexpr int SP = Split<K>::SP, KL = Split<K>::KL;
@@ -134,7 +149,8 @@ VDFCG_DEV void em_pass(const Src& src, int n, EmState<D, K>& S, double* red) {
   // the max and the sum of the log-sum-exp are combined with SP-lane xor shuffles. The
   // loop is warp-uniform (a missing point gets weight 0 and adds nothing). Slots >= m
   // carry cst = -inf, A = b = 0, so they add exactly nothing and are never read.
-  for (int b0 = warp * GPW; b0 < n; b0 += G * GPW) {
+  const int crank = cluster_rank<CL>(), cn = cluster_size<CL>();
+  for (int b0 = (crank * G + warp) * GPW; b0 < n; b0 += cn * G * GPW) {
     const int p = b0 + lane / SP;
     const bool valid = p < n;
     double z[D], w;
@@ -248,21 +264,22 @@ VDFCG_DEV void em_pass(const Src& src, int n, EmState<D, K>& S, double* red) {
     if (lane == 0) red[warp * W + K * NS] = v;
   }
   }
-  __syncthreads();
+  if constexpr (CL) cooperative_groups::this_cluster().sync();  // every CTA's partials visible
+  else __syncthreads();
   for (int t = threadIdx.x; t < W; t += blockDim.x) {
-    if (t < K * NS) {
-      const int i = t / NS;
-      if (i >= m) continue;
-      double sum = 0.0;
-      for (int g = 0; g < G; ++g) sum += red[g * W + t];
-      if (EXACT) S.st2[i][t % NS] = sum; else S.st[i][t % NS] = sum;
-    } else if (!EXACT) {
-      double sum = 0.0;
-      for (int g = 0; g < G; ++g) sum += red[g * W + t];
-      S.ll = sum;
+    if (t >= K * NS ? EXACT : t / NS >= m) continue;
+    double sum = 0.0;
+    for (int r = 0; r < cn; ++r) {  // CTAs in rank order, then warps: fixed summation order
+      const double* rr = red;
+      if constexpr (CL) rr = cooperative_groups::this_cluster().map_shared_rank(red, r);
+      for (int g = 0; g < G; ++g) sum += rr[g * W + t];
     }
+    if (t >= K * NS) S.ll = sum;
+    else if (EXACT) S.st2[t / NS][t % NS] = sum;
+    else S.st[t / NS][t % NS] = sum;
   }
-  __syncthreads();
+  if constexpr (CL) cooperative_groups::this_cluster().sync();  // remote reads done
+  else __syncthreads();
 }
 
 // FP32 E-step mode (FitConfig.estep_fp32, tolerance 1e-4): log-densities, the
@@ -400,9 +417,10 @@ VDFCG_DEV EmConfig cell_config(const EmConfig& cfg, int c) {
 }
 
 // ---------------------------------------------------------------- the fit
-template <int D, int K, bool F32, class Src>
+template <int D, int K, bool F32, bool CL, class Src>
 VDFCG_DEV void run_fit(const Src& src, int n, EmState<D, K>& S, double* red, const EmConfig& cfg,
                        const EmOut& out, int c) {
+  const bool writer = cluster_rank<CL>() == 0;  // one CTA of a cluster writes the results
   constexpr int NS = NStat<D>::value;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // ---- init (wgmm.cpp:136-191)
@@ -469,7 +487,7 @@ VDFCG_DEV void run_fit(const Src& src, int n, EmState<D, K>& S, double* red, con
 
     // ---- E-step + sufficient statistics (one pass over the points)
     if constexpr (F32) em_pass_f32<D, K>(src, n, S, red);
-    else em_pass<D, K, false>(src, n, S, red);
+    else em_pass<D, K, false, CL>(src, n, S, red);
 
     // ---- M-step part 1 (wgmm.cpp:269-298)
     if (warp == 0) {
@@ -523,13 +541,13 @@ VDFCG_DEV void run_fit(const Src& src, int n, EmState<D, K>& S, double* red, con
     __syncthreads();
     if (S.status) break;
     if (S.exact_mask) {
-      if (threadIdx.x == 0 && cfg.exact_counter) atomicAdd(cfg.exact_counter, 1ull);
+      if (threadIdx.x == 0 && writer && cfg.exact_counter) atomicAdd(cfg.exact_counter, 1ull);
       if (warp == 0 && lane < S.m && ((S.exact_mask >> lane) & 1)) {
 #pragma unroll
         for (int a = 0; a < D; ++a) S.muc[lane][a] = S.mu_new[lane][a];
       }
       __syncthreads();
-      em_pass<D, K, true>(src, n, S, red);
+      em_pass<D, K, true, CL>(src, n, S, red);
     }
 
     // ---- M-step part 2: covariances, collapse test, repair (wgmm.cpp:299-316)
@@ -579,14 +597,14 @@ VDFCG_DEV void run_fit(const Src& src, int n, EmState<D, K>& S, double* red, con
     // ---- protocol: removal, pruning, convergence (wgmm.cpp:383-417), thread 0
     if (threadIdx.x == 0) {
       const double ll = S.ll;
-      if (out.trace && it - 1 < out.trace_cap)
+      if (writer && out.trace && it - 1 < out.trace_cap)
         out.trace[static_cast<int64_t>(c) * out.trace_cap + (it - 1)] = ll;
       const int mask = S.dead_mask | S.degen_mask;
       bool pruned = false;
       for (int i = S.m - 1; i >= 0; --i) {
         if (!((mask >> i) & 1)) continue;
         if (S.m <= 1) break;
-        if (out.ev_it && S.n_events < out.K) {
+        if (writer && out.ev_it && S.n_events < out.K) {
           const int64_t e = static_cast<int64_t>(c) * out.K + S.n_events;
           out.ev_it[e] = it;
           out.ev_comp[e] = i;
@@ -601,7 +619,7 @@ VDFCG_DEV void run_fit(const Src& src, int n, EmState<D, K>& S, double* red, con
         int idx = -1;
         double wgt = 0.0;
         if (prune_one_dev<D>(S.alpha, &S.mu[0][0], &S.cov[0][0], S.m, cfg.prune_thr, &idx, &wgt)) {
-          if (out.ev_it && S.n_events < out.K) {
+          if (writer && out.ev_it && S.n_events < out.K) {
             const int64_t e = static_cast<int64_t>(c) * out.K + S.n_events;
             out.ev_it[e] = it;
             out.ev_comp[e] = idx;
@@ -623,6 +641,7 @@ VDFCG_DEV void run_fit(const Src& src, int n, EmState<D, K>& S, double* red, con
   }
 
   // ---- epilogue: denormalize (wgmm.cpp:102-120) and write
+  if (!writer) return;
   const int K_out = out.K;
   const int64_t base = static_cast<int64_t>(c) * K_out;
   if (S.status == 0) {
@@ -846,15 +865,17 @@ __global__ void __launch_bounds__(256) __maxnreg__(K <= 4 ? 128 : 255) em_kernel
   const int n_cells = KEYS ? kc.n_cells : 1;
   for (int j = threadIdx.x; j < kExpTab; j += blockDim.x) S.exp2tab[j] = kExp2Tab[j];
   for (int j = threadIdx.x; j < 256; j += blockDim.x) S.logtab[j] = kLogTab[j];
-  for (;;) {
-    if (threadIdx.x == 0) S.cell = atomicAdd(counter, 1);
+  for (int pass = 0;; ++pass) {
+    // cells: persistent CTAs pull fits from a queue; a single fit (!KEYS) is processed once
+    // by every CTA of the cluster
+    if (KEYS && threadIdx.x == 0) S.cell = atomicAdd(counter, 1);
     __syncthreads();
-    const int c = S.cell;
+    const int c = KEYS ? S.cell : pass;
     if (c >= n_cells) break;
     if (KEYS) {
       KeySrc<D> src;
       const int n = key_prologue<D, K>(kc, c, cfg, S, ztab, red, src);
-      run_fit<D, K, F32>(src, n, S, red, cfg, out, c);
+      run_fit<D, K, F32, false>(src, n, S, red, cfg, out, c);
     } else {
       if (threadIdx.x == 0) {
         S.fr = *ca.frame;
@@ -864,7 +885,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(K <= 4 ? 128 : 255) em_kernel
       __syncthreads();
       CoordSrc<D> src{ca.z, ca.n, ca.w};
       if (S.status) {
-        if (threadIdx.x == 0) {
+        if (threadIdx.x == 0 && cluster_rank<!KEYS>() == 0) {
           out.status[c] = S.status;
           out.comps[c] = 0;
           out.iters[c] = 0;
@@ -875,7 +896,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(K <= 4 ? 128 : 255) em_kernel
           if (out.err_value) out.err_value[c] = S.fr.err_value;
         }
       } else {
-        run_fit<D, K, false>(src, static_cast<int>(ca.n), S, red, cfg, out, c);
+        run_fit<D, K, false, !KEYS>(src, static_cast<int>(ca.n), S, red, cfg, out, c);
       }
     }
     __syncthreads();
@@ -896,11 +917,31 @@ void launch_em_tf(vdfcg_ctx* ctx, const KeyCells& kc, const CoordArgs& ca,
   int occ = 0;
   VDFCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, G * 32, smem));
   if (occ < 1) throw CudaError("EM kernel cannot be resident (registers/shared memory)");
-  const int grid = std::max(1, std::min(n_cells, ctx->sm_count * occ));
   int* counter = arena<int>(ctx, 1);
   VDFCG_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), ctx->stream));
-  VDFCG_LAUNCH(ctx, "em_fit",
-               k<<<grid, G * 32, smem, ctx->stream>>>(kc, ca, cfg, out, counter, red_stride));
+  if constexpr (!KEYS) {
+    // one fit: a cluster of CTAs, ~4 points per lane each, at most 16 (non-portable size)
+    const int64_t per_cta = int64_t(G) * 32 * 4;
+    const int cl = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(1, (ca.n + per_cta - 1) / per_cta)));
+    if (cl > 8) VDFCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(cl);
+    lc.blockDim = dim3(G * 32);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    VDFCG_LAUNCH(ctx, "em_fit", cudaLaunchKernelEx(&lc, k, kc, ca, cfg, out, counter, red_stride));
+  } else {
+    const int grid = std::max(1, std::min(n_cells, ctx->sm_count * occ));
+    VDFCG_LAUNCH(ctx, "em_fit",
+                 k<<<grid, G * 32, smem, ctx->stream>>>(kc, ca, cfg, out, counter, red_stride));
+  }
 }
 
 template <int D, int K, bool KEYS>
