@@ -53,11 +53,7 @@ VDFCG_DEV bool prep_component(double* cov9, double alpha, double* Lo, double* rd
   return true;
 }
 
-#ifndef VDFCG_EXPTAB
-#define VDFCG_EXPTAB 256
-#endif
-constexpr int kExpTab = VDFCG_EXPTAB;  // 64 (degree-5 polynomial) or 256 (degree 4)
-#if VDFCG_EXPTAB == 256
+constexpr int kExpTab = 256;
 // 2^(j/256), j = 0..255, correctly rounded (50-digit decimal evaluation).
 __device__ __constant__ double kExp2Tab[256] = {
     1.0, 1.0027112750502025, 1.0054299011128027, 1.0081558981184175,
@@ -125,79 +121,14 @@ __device__ __constant__ double kExp2Tab[256] = {
     1.9571441241754002, 1.9624504802089273, 1.9677712232331759, 1.9731063922552343,
     1.978456026387951, 1.9838201648502194, 1.9891988469672663, 1.9945921121709402};
 
-__device__ __constant__ double kExpC[8] = {
-    369.3299304675746, 6755399441055744.0, 0.0027076061740622863, 9.0587766165871078e-20,
-    1.0 / 24.0, 1.0 / 6.0, 0.5, 1.0};
-#else
-// 2^(j/64), j = 0..63, correctly rounded (50-digit decimal evaluation).
-__device__ __constant__ double kExp2Tab[64] = {
-    1.0, 1.0108892860517005, 1.0218971486541166, 1.0330248790212284,
-    1.0442737824274138, 1.0556451783605572, 1.0671404006768237, 1.0787607977571199,
-    1.0905077326652577, 1.102382583307841, 1.1143867425958924, 1.1265216186082418,
-    1.1387886347566916, 1.1511892299529827, 1.1637248587775775, 1.1763969916502812,
-    1.189207115002721, 1.202156731452703, 1.215247359980469, 1.22848053610687,
-    1.241857812073484, 1.255380757024691, 1.2690509571917332, 1.2828700160787783,
-    1.2968395546510096, 1.3109612115247644, 1.3252366431597413, 1.339667524053303,
-    1.3542555469368927, 1.3690024229745905, 1.383909881963832, 1.3989796725383112,
-    1.4142135623730951, 1.42961333839197, 1.4451808069770467, 1.460917794180647,
-    1.4768261459394993, 1.4929077282912648, 1.5091644275934228, 1.5255981507445384,
-    1.5422108254079407, 1.559004400237837, 1.5759808451078865, 1.593142151342267,
-    1.6104903319492543, 1.6280274218573478, 1.645755478153965, 1.6636765803267364,
-    1.681792830507429, 1.7001063537185235, 1.718619298122478, 1.7373338352737062,
-    1.7562521603732995, 1.7753764925265212, 1.7947090750031072, 1.8142521755003989,
-    1.8340080864093424, 1.8539791250833855, 1.8741676341103, 1.8945759815869656,
-    1.9152065613971474, 1.9360617934922943, 1.9571441241754002, 1.978456026387951};
-__device__ __constant__ double kExpC[9] = {
-    92.33248261689366,        // 64 / ln 2
-    6755399441055744.0,       // 1.5 * 2^52 (round-to-nearest-integer shifter)
-    0.010830424696249145,     // ln2/64, high part
-    3.6235106466348431e-19,   // ln2/64, low part
-    1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 0.5, 1.0};
-#endif
 
-// exp(x) for x <= 709, accurate to ~1 ulp: x = (T q + j) ln2/T + r with |r| <= ln2/(2T)
-// (FMA Cody-Waite), 2^(j/T) from a T-entry shared table, Taylor for e^r (truncation
-// < 4e-17). The FP64 constants live in the constant bank (c[][] operands, no per-call
-// literal materialisation). x is clamped at -708 (e^-708 ~ 3e-308: such terms are below
-// every tolerance; the E-step falls back to the max-shifted sum when a whole mixture
-// underflows).
-VDFCG_DEV double exp_nonpos(double x, const double* tab) {
-  x = x < -708.0 ? -708.0 : x;  // compare-select (fmax's IEEE NaN handling costs ~10 instr)
-  const double tm = fma(x, kExpC[0], kExpC[1]);
-  const int k = __double2loint(tm);
-  const double kd = tm - kExpC[1];
-  double r = fma(-kd, kExpC[2], x);
-  r = fma(-kd, kExpC[3], r);
-#if VDFCG_EXPTAB == 256
-  double p = fma(r, kExpC[4], kExpC[5]);
-  p = fma(p, r, kExpC[6]);
-  p = fma(p, r, kExpC[7]);
-  p = fma(p, r, 1.0);
-  constexpr int SH = 8;
-#else
-  double p = fma(r, kExpC[4], kExpC[5]);
-  p = fma(p, r, kExpC[6]);
-  p = fma(p, r, kExpC[7]);
-  p = fma(p, r, kExpC[8]);
-  p = fma(p, r, 1.0);
-  constexpr int SH = 6;
-#endif
-  // 2^q by an integer add to the exponent field of tab*p (in [0.99, 2)): one DMUL less.
-  // At the -708 clamp the result may lose normality; it is < 1e-307 there either way.
-  const double v = tab[k & (kExpTab - 1)] * p;
-  return __hiloint2double(__double2hiint(v) + ((k >> SH) << 20), __double2loint(v));
-}
-
-// Log2-domain E-step (VDFCG_LOG2=1, default): the affine form is pre-scaled by
+// Log2-domain E-step: the affine form is pre-scaled by
 // sqrt(log2(e)/2) and cst by log2(e), so a component's term is
 //   lp2 = cst2 - |A2 z - b2|^2 = log2(e) * (cst - |A z - b|^2 / 2)
 // (three FMAs from cst, no separate -0.5 scaling) and 2^x needs no ln2 multiply: the
 // table index comes straight from x * 256 and the reduced argument x - k/256 is exact, so
 // the two-constant Cody-Waite step collapses to one FMA. e^(r ln 2) by a degree-4 Taylor
 // polynomial in r (|r| <= 1/512: truncation < 4e-17).
-#ifndef VDFCG_LOG2
-#define VDFCG_LOG2 1
-#endif
 __device__ __constant__ double kExp2C[7] = {
     256.0, 6755399441055744.0, 0.00390625,
     0.0096181291076284772,   // ln2^4 / 24

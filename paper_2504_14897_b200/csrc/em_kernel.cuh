@@ -20,22 +20,10 @@ struct NStat {
   static constexpr int value = 1 + D + D * (D + 1) / 2;
 };
 
-// Lanes per point in the point pass (component split, see em_pass). 2 for K in 2..4:
-// each lane of a pair owns K/2 components' accumulators, halving the registers.
-#ifndef VDFCG_SPLIT
-#define VDFCG_SPLIT 1
-#endif
-template <int K>
-struct Split {
-  static constexpr int SP = (K >= 2 && K <= 4) ? VDFCG_SPLIT : 1;
-  static constexpr int KL = (K + SP - 1) / SP;  // component slots per lane
-  static constexpr int KPAD = KL * SP;          // padded slot count
-};
-
 template <int D, int K>
 struct EmState {
   static constexpr int NS = NStat<D>::value;
-  static constexpr int KP = Split<K>::KPAD;
+  static constexpr int KP = K;
   double alpha[K];
   double mu[K][D];
   double cov[K][9];
@@ -130,66 +118,42 @@ VDFCG_DEV int cluster_size() {
 template <int D, int K, bool EXACT, bool CL, class Src>
 VDFCG_DEV void em_pass(const Src& src, int n, EmState<D, K>& S, double* red) {
   constexpr int NS = NStat<D>::value;
-  constexpr int SP = Split<K>::SP, KL = Split<K>::KL;
   const int m = S.m;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, G = blockDim.x >> 5;
-  const int part = lane % SP;       // this lane owns slots [part*KL, part*KL + KL)
-  const int slot0 = part * KL;
-  constexpr int GPW = 32 / SP;      // points per warp per iteration
-  double acc[KL][NS];
+  constexpr int GPW = 32;  // points per warp per iteration (one per lane)
+  double acc[K][NS];
 #pragma unroll
-  for (int j = 0; j < KL; ++j)
+  for (int j = 0; j < K; ++j)
 #pragma unroll
     for (int t = 0; t < NS; ++t) acc[j][t] = 0.0;
   // Per-lane plain sum + the fixed-order tree below: the reference's Kahan sum
   // (gaussian.hpp:55-68) guards one sequential sum over all points; the error here stays
   // ~1e-15 relative either way.
   double ll = 0.0;
-  // Each point is owned by SP adjacent lanes, each evaluating its own KL component slots;
-  // the max and the sum of the log-sum-exp are combined with SP-lane xor shuffles. The
-  // loop is warp-uniform (a missing point gets weight 0 and adds nothing). Slots >= m
-  // carry cst = -inf, A = b = 0, so they add exactly nothing and are never read.
+  // One point per lane, all K component slots. The loop is warp-uniform (a missing point
+  // gets weight 0 and adds nothing). Slots >= m carry cst = -inf, A = b = 0, so they add
+  // exactly nothing and are never read.
   const int crank = cluster_rank<CL>(), cn = cluster_size<CL>();
   for (int b0 = (crank * G + warp) * GPW; b0 < n; b0 += cn * G * GPW) {
-    const int p = b0 + lane / SP;
+    const int p = b0 + lane;
     const bool valid = p < n;
     double z[D], w;
     src.load(valid ? p : b0, z, w);
     if (!valid) w = 0.0;
-    double lp[KL];
+    double lp[K];
     double mx = -dinf();
 #pragma unroll
-    for (int j = 0; j < KL; ++j) {
-      const int i = slot0 + j;
-#if VDFCG_LOG2
-      lp[j] = comp_logp2_affine<D>(z, S.A[i], S.bv[i], S.cst[i]);
-#else
-      lp[j] = comp_logp_affine<D>(z, S.A[i], S.bv[i], S.cst[i]);
-#endif
+    for (int j = 0; j < K; ++j) {
+      lp[j] = comp_logp2_affine<D>(z, S.A[j], S.bv[j], S.cst[j]);
       mx = lp[j] > mx ? lp[j] : mx;
-    }
-#pragma unroll
-    for (int o = 1; o < SP; o <<= 1) {
-      const double other = __shfl_xor_sync(0xffffffffu, mx, o);
-      mx = other > mx ? other : mx;
     }
     double sum = 0.0;
 #pragma unroll
-    for (int j = 0; j < KL; ++j) {
-#if VDFCG_LOG2
+    for (int j = 0; j < K; ++j) {
       lp[j] = exp2_nonpos(lp[j] - mx, S.exp2tab);
-#else
-      lp[j] = exp_nonpos(lp[j] - mx, S.exp2tab);
-#endif
       sum += lp[j];
     }
-#pragma unroll
-    for (int o = 1; o < SP; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-#if VDFCG_LOG2
-    if (!EXACT && part == 0) ll += w * fma(mx, 0.6931471805599453, log_ge1(sum, S.logtab));
-#else
-    if (!EXACT && part == 0) ll += w * (mx + log_ge1(sum, S.logtab));
-#endif
+    if (!EXACT) ll += w * fma(mx, 0.6931471805599453, log_ge1(sum, S.logtab));
     const double ws = w * rcp_newton(sum);
     if (!EXACT) {
       // Pass 1 accumulates about the frame origin (z is the normalised coordinate,
@@ -203,7 +167,7 @@ VDFCG_DEV void em_pass(const Src& src, int n, EmState<D, K>& S, double* red) {
 #pragma unroll
         for (int b2 = a; b2 < D; ++b2) zz[uidx<D>(a, b2)] = z[a] * z[b2];
 #pragma unroll
-      for (int j = 0; j < KL; ++j) {
+      for (int j = 0; j < K; ++j) {
         const double g = lp[j] * ws;
         acc[j][0] += g;
 #pragma unroll
@@ -213,13 +177,12 @@ VDFCG_DEV void em_pass(const Src& src, int n, EmState<D, K>& S, double* red) {
       }
     } else {
 #pragma unroll
-      for (int j = 0; j < KL; ++j) {
-        const int i = slot0 + j;
-        if (!((S.exact_mask >> i) & 1)) continue;
+      for (int j = 0; j < K; ++j) {
+        if (!((S.exact_mask >> j) & 1)) continue;
         const double g = lp[j] * ws;
         double dl[D];
 #pragma unroll
-        for (int a = 0; a < D; ++a) dl[a] = z[a] - S.muc[i][a];
+        for (int a = 0; a < D; ++a) dl[a] = z[a] - S.muc[j][a];
         acc[j][0] += g;
 #pragma unroll
         for (int a = 0; a < D; ++a) {
@@ -231,38 +194,22 @@ VDFCG_DEV void em_pass(const Src& src, int n, EmState<D, K>& S, double* red) {
       }
     }
   }
-  // fixed-order reduction: lanes of the same part (xor tree) -> warps (ascending)
+  // fixed-order reduction: lanes (reduce-scatter) -> warps -> cluster CTAs (ascending)
   constexpr int W = K * NS + 1;
-  if (SP == 1) {  // reduce-scatter: each lane ends with ~2 of the K*NS+1 warp totals
-    double v[KL * NS + 1];
+  {  // reduce-scatter: each lane ends with ~2 of the K*NS+1 warp totals
+    double v[K * NS + 1];
 #pragma unroll
-    for (int j = 0; j < KL; ++j)
+    for (int j = 0; j < K; ++j)
 #pragma unroll
       for (int t = 0; t < NS; ++t) v[j * NS + t] = acc[j][t];
-    v[KL * NS] = EXACT ? 0.0 : ll;
+    v[K * NS] = EXACT ? 0.0 : ll;
     int start, count;
     warp_scatter_sum(v, lane, start, count);
 #pragma unroll
-    for (int j = 0; j < WarpScatter<KL * NS + 1>::HOUT; ++j) {
+    for (int j = 0; j < WarpScatter<K * NS + 1>::HOUT; ++j) {
       const int gi = start + j;
       if (j < count && (gi == K * NS ? !EXACT : gi / NS < m)) red[warp * W + gi] = v[j];
     }
-  } else {
-#pragma unroll
-  for (int j = 0; j < KL; ++j) {
-#pragma unroll
-    for (int t = 0; t < NS; ++t) {
-      double v = acc[j][t];
-#pragma unroll
-      for (int o = 16; o >= SP; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      const int i = slot0 + j;
-      if (lane < SP && i < m) red[warp * W + i * NS + t] = v;
-    }
-  }
-  if (!EXACT) {
-    const double v = warp_sum(ll);
-    if (lane == 0) red[warp * W + K * NS] = v;
-  }
   }
   if constexpr (CL) cooperative_groups::this_cluster().sync();  // every CTA's partials visible
   else __syncthreads();
@@ -327,28 +274,16 @@ VDFCG_DEV void em_pass_f32(const Src& src, int n, EmState<D, K>& S, double* red)
         const float y2 = fmaf(S.Af[i][5], zf[2], fmaf(S.Af[i][4], zf[1], fmaf(S.Af[i][3], zf[0], -S.bf[i][2])));
         q = fmaf(y2, y2, q);
       }
-#if VDFCG_LOG2
       u[i] = S.cstf[i] - q;  // log2 domain (pre-scaled affine form)
-#else
-      u[i] = fmaf(-0.5f, q, S.cstf[i]);
-#endif
       mx = u[i] > mx ? u[i] : mx;
     }
     float sum = 0.0f;
 #pragma unroll
     for (int i = 0; i < KP; ++i) {
-#if VDFCG_LOG2
       u[i] = ex2f_approx(u[i] - mx);
-#else
-      u[i] = ex2f_approx((u[i] - mx) * 1.4426950408889634f);
-#endif
       sum += u[i];
     }
-#if VDFCG_LOG2
     ll += w * (0.6931471805599453 * (static_cast<double>(mx) + static_cast<double>(lg2f_approx(sum))));
-#else
-    ll += w * (static_cast<double>(mx) + 0.6931471805599453 * static_cast<double>(lg2f_approx(sum)));
-#endif
     const float inv = __frcp_rn(sum);
     double zz[D * (D + 1) / 2];
 #pragma unroll
@@ -366,17 +301,20 @@ VDFCG_DEV void em_pass_f32(const Src& src, int n, EmState<D, K>& S, double* red)
     }
   }
   constexpr int W = K * NS + 1;
+  {  // reduce-scatter (as in em_pass)
+    double v[K * NS + 1];
 #pragma unroll
-  for (int i = 0; i < KP; ++i) {
+    for (int j = 0; j < K; ++j)
 #pragma unroll
-    for (int t = 0; t < NS; ++t) {
-      const double v = warp_sum(acc[i][t]);
-      if (lane == 0 && i < m) red[warp * W + i * NS + t] = v;
+      for (int t = 0; t < NS; ++t) v[j * NS + t] = acc[j][t];
+    v[K * NS] = ll;
+    int start, count;
+    warp_scatter_sum(v, lane, start, count);
+#pragma unroll
+    for (int j = 0; j < WarpScatter<K * NS + 1>::HOUT; ++j) {
+      const int gi = start + j;
+      if (j < count && (gi == K * NS || gi / NS < m)) red[warp * W + gi] = v[j];
     }
-  }
-  {
-    const double v = warp_sum(ll);
-    if (lane == 0) red[warp * W + K * NS] = v;
   }
   __syncthreads();
   for (int t = threadIdx.x; t < W; t += blockDim.x) {
@@ -444,13 +382,11 @@ VDFCG_DEV void run_fit(const Src& src, int n, EmState<D, K>& S, double* red, con
       if (lane < S.m) {
         dead = !prep_component<D>(S.cov[lane], S.alpha[lane], S.Lo[lane], S.rd[lane], &S.cst[lane]);
         affine_from_chol<D>(S.mu[lane], S.Lo[lane], S.rd[lane], S.A[lane], S.bv[lane]);
-#if VDFCG_LOG2
 #pragma unroll
         for (int e = 0; e < 6; ++e) S.A[lane][e] *= kSqrtHalfLog2E;
 #pragma unroll
         for (int a = 0; a < 3; ++a) S.bv[lane][a] *= kSqrtHalfLog2E;
         S.cst[lane] *= kLog2E;
-#endif
 #pragma unroll
         for (int a = 0; a < D; ++a) S.muc[lane][a] = S.mu[lane][a];
 #pragma unroll
