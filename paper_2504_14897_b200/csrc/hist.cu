@@ -722,6 +722,7 @@ __global__ void __launch_bounds__(BLOCK) cells_bitmap_tma_kernel(
   unsigned* wpre = bitmap + words;                                       // [words]
   unsigned* cnt = wpre + words;                                          // [ccap]
   unsigned* kbuf = cnt + ccap;                                           // [capp]
+  unsigned* keyr = kbuf + capp;                                          // [ccap] key of rank r
   const int wpt = (words + BLOCK - 1) / BLOCK;
   const int64_t lim = offsets[n_cells];
   for (int t = threadIdx.x; t < words; t += BLOCK) bitmap[t] = 0u;
@@ -781,19 +782,21 @@ __global__ void __launch_bounds__(BLOCK) cells_bitmap_tma_kernel(
       }
     }
     __syncthreads();
-    // 3. counts per rank, keys at their rank
+    // 3. counts per rank; each rank's key goes to shared memory (the scattered global
+    //    stores of the key per particle cost ~10% of the kernel), emitted coalesced below
     for (int li = threadIdx.x; li < nc; li += BLOCK) {
       const unsigned key = kbuf[li];
       if (key != 0xffffffffu) {
         const unsigned wd = key >> 5, bit = key & 31;
         const unsigned r = wpre[wd] + __popc(bitmap[wd] & ((1u << bit) - 1u));
         atomicAdd(cnt + r, 1u);
-        keys_out[b + r] = key;
+        keyr[r] = key;  // duplicates store the same value
       }
     }
     __syncthreads();
     // 4. emit counts, re-zero
-    for (unsigned r = threadIdx.x; r < total; r += BLOCK) {
+    for (unsigned r = threadIdx.x; r < total; r += BLOCK) {  // coalesced keys + counts
+      keys_out[b + r] = keyr[r];
       counts_out[b + r] = static_cast<double>(cnt[r]);
       cnt[r] = 0u;
     }
@@ -921,7 +924,7 @@ static void bin_cells_d(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
   // TMA-staged variant: every axis base 16-byte aligned and the staging buffer (largest
   // cell + 16-byte slack per axis) fits beside the bitmap with two CTAs per SM.
   const int64_t capp = ((maxc + 2 + 1) / 2) * 2;
-  const size_t tma_smem = size_t(D) * capp * 8 + size_t(words) * 8 + size_t(ccap) * 4 + size_t(capp) * 4;
+  const size_t tma_smem = size_t(D) * capp * 8 + size_t(words) * 8 + size_t(ccap) * 8 + size_t(capp) * 4;
   bool aligned = true;
   for (int a = 0; a < D; ++a) aligned = aligned && (reinterpret_cast<uintptr_t>(c.vel[a]) & 15) == 0;
   static const int tma_env = [] {
