@@ -113,8 +113,11 @@ def test_determinism_bitwise():
     _, r1, rec1, _ = G.compress_cells(b, cfg, meta)
     _, r2, rec2, _ = G.compress_cells(b, cfg, meta)
     assert torch.equal(rec1, rec2)
-    for f in ("weights", "means", "covariances", "final_loglik", "iterations"):
-        assert torch.equal(getattr(r1, f), getattr(r2, f))
+    for f in ("weights", "means", "covariances", "final_loglik", "iterations", "status"):
+        a, b2 = getattr(r1, f), getattr(r2, f)
+        if a.dtype == torch.float64:  # bit patterns (NaN-safe)
+            a, b2 = a.view(torch.int64), b2.view(torch.int64)
+        assert torch.equal(a, b2), f
 
 
 def test_cfg4_scale_properties():
@@ -247,3 +250,25 @@ def test_pipelined_host_path_bitwise_equals_device_path():
             used = torch.arange(4)[None, :] < rh.components[:, None].long()
             a, b = a[used], b[used]
         assert torch.equal(a, b), f
+
+
+def test_pipelined_host_path_weighted_bitwise():
+    """Weighted particles through the chunked host-input path == device-resident path."""
+    import torch
+    dev = torch.device("cuda", 0)
+    n_cells, per = 2500, 1800
+    offs = torch.arange(n_cells + 1, dtype=torch.int64, device=dev) * per
+    axes = [torch.empty(n_cells * per, dtype=torch.float64, device=dev) for _ in range(3)]
+    G.synth_cells(3, offs, 17, 1, *axes)
+    w = torch.rand(n_cells * per, dtype=torch.float64, device=dev, generator=torch.Generator(dev).manual_seed(3)) * 3.0 + 0.1
+    cfg = FitConfig(initial_components=3, seed=5, temperature=np.ones(3))
+    meta = ModelMeta("i", None, 2, [AxisRange(-6, 6)] * 3)
+    _, rd, recd, _ = G.compress_cells(G.CellBatch(axes, offs, 40, [-6] * 3, [6] * 3, w), cfg, meta)
+    hb = G.CellBatch([a.cpu().pin_memory() for a in axes], offs.cpu(), 40, [-6] * 3, [6] * 3,
+                     w.cpu().pin_memory())
+    assert hb.n >= (1 << 22)  # large enough for the pipelined path
+    _, rh, rech, _ = G.compress_cells(hb, cfg, meta)
+    assert torch.equal(recd.cpu(), rech)
+    for f in ("status", "components", "iterations"):
+        assert torch.equal(getattr(rd, f).cpu(), getattr(rh, f)), f
+    assert torch.equal(rd.weights.cpu().view(torch.int64), rh.weights.view(torch.int64))
