@@ -552,7 +552,7 @@ def main():
     ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-cells", type=int, default=2048, help="CPU-baseline sample cells/species")
-    ap.add_argument("--cpu-repeats", type=int, default=3, help="CPU-baseline repeats (median)")
+    ap.add_argument("--cpu-repeats", type=int, default=5, help="CPU-baseline repeats (median, SURVEY 8(d))")
     ap.add_argument("--ref-cells", type=int, default=256, help="reference arm cells/species/step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
