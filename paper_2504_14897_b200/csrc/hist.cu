@@ -707,7 +707,7 @@ VDFCG_DEV void issue_cell_copy(const VelPtrs& vp, const int64_t* offsets, int c,
     for (int a = 0; a < D; ++a) bulk_g2s(pbuf + a * capp, vp.v[a] + b0, bytes, bar);
 }
 
-template <int D, int BLOCK>
+template <int D, int BLOCK, int kTmaWpt>  // kTmaWpt >= bitmap words per thread
 __global__ void __launch_bounds__(BLOCK) cells_bitmap_tma_kernel(
     VelPtrs vp, const int64_t* __restrict__ offsets, int n_cells, CellGeom g, int words, int ccap,
     int capp, int32_t* nnz, uint32_t* __restrict__ keys_out, double* __restrict__ counts_out,
@@ -766,20 +766,20 @@ __global__ void __launch_bounds__(BLOCK) cells_bitmap_tma_kernel(
     // the staging buffer is free: fetch the next cell while this one is ranked
     if (threadIdx.x == 0 && c + static_cast<int>(gridDim.x) < n_cells)
       issue_cell_copy<D>(vp, offsets, c + gridDim.x, lim, pbuf, capp, &bar);
-    // 2. ranks
-    unsigned local = 0;
-    for (int k = 0; k < wpt; ++k) {
+    // 2. ranks; the word popcounts stay in registers for the prefix and the re-zeroing
+    unsigned local = 0, pc[kTmaWpt];
+#pragma unroll
+    for (int k = 0; k < kTmaWpt; ++k) {
       const int wi = threadIdx.x * wpt + k;
-      if (wi < words) local += __popc(bitmap[wi]);
+      pc[k] = (k < wpt && wi < words) ? __popc(bitmap[wi]) : 0u;
+      local += pc[k];
     }
     unsigned pre, total;
     Scan(ss).ExclusiveSum(local, pre, total);
-    for (int k = 0; k < wpt; ++k) {
-      const int wi = threadIdx.x * wpt + k;
-      if (wi < words) {
-        wpre[wi] = pre;
-        pre += __popc(bitmap[wi]);
-      }
+#pragma unroll
+    for (int k = 0; k < kTmaWpt; ++k) {
+      if (pc[k]) wpre[threadIdx.x * wpt + k] = pre;  // only occupied words are ever read
+      pre += pc[k];
     }
     __syncthreads();
     // 3. counts per rank; each rank's key goes to shared memory (the scattered global
@@ -800,7 +800,9 @@ __global__ void __launch_bounds__(BLOCK) cells_bitmap_tma_kernel(
       counts_out[b + r] = static_cast<double>(cnt[r]);
       cnt[r] = 0u;
     }
-    for (int t = threadIdx.x; t < words; t += BLOCK) bitmap[t] = 0u;
+#pragma unroll
+    for (int k = 0; k < kTmaWpt; ++k)
+      if (pc[k]) bitmap[threadIdx.x * wpt + k] = 0u;
     if (threadIdx.x == 0) {
       const unsigned to = s_oor;
       nnz[c] = static_cast<int32_t>(total);
@@ -932,8 +934,10 @@ static void bin_cells_d(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
     return e ? atoi(e) : 1;
   }();
   const int tb = tma_env == 2 ? 256 : 512;
-  if (!weighted && sparse && aligned && tma_env && tma_smem <= 110 * 1024) {
-    auto k = tb == 512 ? cells_bitmap_tma_kernel<D, 512> : cells_bitmap_tma_kernel<D, 256>;
+  if (!weighted && sparse && aligned && tma_env && tma_smem <= 110 * 1024 && words <= 16 * tb) {
+    const bool w8 = words <= 8 * tb;
+    auto k = tb == 512 ? (w8 ? cells_bitmap_tma_kernel<D, 512, 8> : cells_bitmap_tma_kernel<D, 512, 16>)
+                       : (w8 ? cells_bitmap_tma_kernel<D, 256, 8> : cells_bitmap_tma_kernel<D, 256, 16>);
     VDFCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tma_smem)));
     int occ = 0;
     VDFCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, tb, tma_smem));

@@ -139,6 +139,7 @@ def _cells_case(d, n_cells, per_cell, n_bins, seed=1, weighted=False):
 @pytest.mark.parametrize("d,n_cells,per_cell,n_bins,weighted", [
     (3, 16, 3000, 32, False),    # dense shared-memory path
     (3, 64, 1900, 48, False),    # sparse bitmap path, TMA-staged (cfg4 shape)
+    (3, 48, 1900, 64, False),    # TMA-staged, 8192 bitmap words (16 per thread)
     (3, 32, 1900, 48, True),     # weighted: sort path, bit-exact sequential sums
     (2, 8, 50000, 64, False),    # 2V dense
     (3, 4, 20000, 64, False),    # dense global path
