@@ -135,6 +135,17 @@ def ncu_traffic(config_name):
         return {}
 
 
+def ncu_pipes(config_name):
+    """FP64-pipe / issue utilisation of each kernel from the same committed capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", f"ncu_traffic_{config_name}.json")) as f:
+            d = json.load(f)
+        return {k: {"fp64_pipe_pct": v.get("fp64_pipe_pct"), "issue_active_pct": v.get("issue_active_pct")}
+                for k, v in d["kernels"].items()}
+    except Exception:
+        return {}
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -430,6 +441,7 @@ def run_gpu(args, cfg):
         roofline = {"kernel": "em_fit", "bound": "fp64", "achieved": ach, "peak": fp64_peak,
                     "unit": "TFLOP/s", "frac": ach / fp64_peak if fp64_peak else None,
                     "traffic": traffic.get("em_fit"), "peak_source": "measured FP64 FMA probe on this GPU (vdfcg_probe_peaks)",
+                    "ncu_pipes": ncu_pipes(args.config).get("em_fit"),
                     "flops_per_launch": em_flops_launch, "avg_launch_ms": em_ms / em_n,
                     "share_of_step": em_ms / max(ms_total if world == 1 else ms_total, 1e-9),
                     "algorithm": f"F(d)={F_D[d]} flops per (point, component, iteration); "
@@ -439,7 +451,7 @@ def run_gpu(args, cfg):
         ach = (hist_bytes * steps) / (h_ms * 1e-3) / 1e9
         roofline_hist = {"kernel": hist_name, "bound": "hbm", "achieved": ach, "peak": hbm_peak,
                          "unit": "GB/s", "frac": ach / hbm_peak,
-                         "traffic": traffic.get(hist_name.replace("cells_", "cells_")) if hist_name else None,
+                         "traffic": traffic.get(hist_name) if hist_name else None,
                          "peak_source": hbm_src, "bytes_per_launch": hist_bytes / len(batches),
                          "avg_launch_ms": h_ms / h_n,
                          "algorithm": "24 B/particle read (u,v,w f64) + 12 B per non-empty bin "
