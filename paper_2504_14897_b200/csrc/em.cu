@@ -1,20 +1,23 @@
 // em.cu — K5: the batched weighted-EM fitter (sm_100a, FP64 CUDA cores).
 //
-// One CTA of G warps owns one fit (a spatial cell, or the single point set of
-// vdfcg_fit) at a time and pulls the next one from an atomic queue (persistent grid).
+// Cells: one CTA of G warps owns one fit at a time and pulls the next one from an
+// atomic queue (persistent grid). A single point set (vdfcg_fit) runs on a thread-block
+// cluster of up to 16 CTAs that split its points and combine partial statistics through
+// distributed shared memory; every CTA runs the same deterministic protocol.
 // Per fit, entirely on-device (wgmm.cpp:364-423):
 //   prologue   normalize over the non-empty bins (wgmm.cpp:78-100), temperature
 //              (wgmm.cpp:22-25), seeded init or warm start (wgmm.cpp:136-191)
 //   iteration  lanes of warp 0 factor every component (LLT + in-place repair,
-//              wgmm.cpp:197-229); all threads stream the points once: log-density via
-//              the Cholesky factor, per-point log-sum-exp, responsibilities and the
-//              weighted sufficient statistics (mass, sum g(x-mu_old), sum g(x-mu_old)^2)
-//              in registers; fixed-order warp-shuffle + cross-warp reduction (bitwise
-//              reproducible); M-step per component lane (Eq. 9 with the NEW mean via the
-//              shifted sums; an exact second pass centred on the new mean when the shift
-//              would cost precision, see need_exact below), collapse test + repair
-//              (wgmm.cpp:300-315); thread 0 runs degenerate removal, scheduled pruning
-//              and the convergence test (wgmm.cpp:386-417) on the E-step log-likelihood
+//              wgmm.cpp:197-229) into a pre-scaled affine form; all threads stream the
+//              points once: log2-domain log-densities, per-point log-sum-exp (table exp2 /
+//              log), responsibilities and the weighted sufficient statistics about the
+//              frame origin in registers; fixed-order warp reduce-scatter + cross-warp
+//              (+ cross-CTA) reduction (bitwise reproducible); M-step per component lane
+//              (Eq. 9; an exact second pass centred on the new mean where the raw-moment
+//              form would cost precision), collapse test by a Cholesky-determinant
+//              certificate with the full eigen/repair path near the threshold
+//              (wgmm.cpp:300-315); thread 0 runs degenerate removal, scheduled pruning and
+//              the convergence test (wgmm.cpp:386-417) on the E-step log-likelihood
 //   epilogue   denormalize (wgmm.cpp:102-120) and write parameters + diagnostics.
 // Points never leave L1/L2 between iterations of a fit; parameters live in shared memory.
 #include <cub/block/block_reduce.cuh>
