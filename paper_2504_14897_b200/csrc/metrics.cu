@@ -194,8 +194,10 @@ __global__ void __launch_bounds__(kMB) cell_metrics_kernel(CellsDev c, CellBinsD
     // monotonically, so nothing overflows), re-anchoring with a direct exp every 32
     // bins (relative error ~32^2 eps); a direction stops once its anchor underflows.
     for (int64_t item = threadIdx.x; item < rows * M; item += kMB) {
-      const int64_t row = item / M;
-      const int k = static_cast<int>(item % M);
+      // component-major items: the lanes of a warp walk consecutive rows of one component,
+      // whose walk lengths (distance from the component's centre) are similar
+      const int k = static_cast<int>(item / rows);
+      const int64_t row = item - k * rows;
       double x[3];
       lead_coords<D>(row, nb, lo, dx, x);
       double base, lin, q0;
@@ -312,15 +314,25 @@ __global__ void __launch_bounds__(kMB) cell_metrics_kernel(CellsDev c, CellBinsD
         x[a] = __dadd_rn(lo[a], __dmul_rn(static_cast<double>(i) + 0.5, dx[a]));
       }
       double lg[kMaxK];
-      double q = 0.0, mx = -dinf();
+      double q = 0.0;
       for (int k = 0; k < M; ++k) {
         lg[k] = log_gauss<D>(comp[k], x);
         q += comp[k].w * exp(lg[k]);
-        mx = fmax(mx, lg[k] + comp[k].logw);
       }
-      double s = 0.0;
-      for (int k = 0; k < M; ++k) s += exp(lg[k] + comp[k].logw - mx);
-      acc[6] += cnt * (mx + log(s));
+      // log sum_k w_k N_k = log q while q is a normal number (the reference's max-shifted
+      // log-sum-exp, wgmm.cpp:262-264, equals it to rounding); the shifted form only
+      // where q underflows
+      double lse;
+      if (q > 1e-290) {
+        lse = log(q);
+      } else {
+        double mx = -dinf();
+        for (int k = 0; k < M; ++k) mx = fmax(mx, lg[k] + comp[k].logw);
+        double s = 0.0;
+        for (int k = 0; k < M; ++k) s += exp(lg[k] + comp[k].logw - mx);
+        lse = mx + log(s);
+      }
+      acc[6] += cnt * lse;
       const double pn = (cnt / zp) * area;
       const double qn = (q / zq) * area;
       if (qn > 0.0) {
