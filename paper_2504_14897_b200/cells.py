@@ -43,6 +43,22 @@ def _empty(like, shape, kind: str):
     return np.empty(shape, dtype=dt)
 
 
+def _ctx(*arrays):
+    """The calling thread's library context, ordered with torch: when any argument is a
+    CUDA tensor the context runs on that device's *current torch stream*, so the
+    library's kernels follow the ops that produced the inputs and precede the ops that
+    consume the outputs (no host synchronisation needed). Host (numpy) calls are
+    synchronous."""
+    api = _api()
+    for a in arrays:
+        if _is_torch(a) and a.is_cuda:
+            import torch
+            ctx = api.context(a.device.index)
+            ctx.set_stream(torch.cuda.current_stream(a.device).cuda_stream)
+            return ctx
+    return api.context()
+
+
 def _api():
     from . import api
     return api
@@ -172,7 +188,7 @@ def bin_cells(batch: CellBatch, out: Optional[CellBins] = None) -> CellBins:
     api = _api()
     out = out or CellBins.alloc(batch)
     bs = out.struct()
-    _check(api.lib().vdfcg_bin_cells(api.context().handle, C.byref(batch.struct), C.byref(bs)))
+    _check(api.lib().vdfcg_bin_cells(_ctx(batch.axes[0]).handle, C.byref(batch.struct), C.byref(bs)))
     return out
 
 
@@ -191,7 +207,7 @@ def fit_cells(batch: CellBatch, bins: CellBins, config: FitConfig, trace: bool =
     bs = bins.struct()
     rs = out.struct()
     ws = warm.struct() if warm is not None else None
-    _check(api.lib().vdfcg_fit_cells_warm(api.context().handle, C.byref(batch.struct), C.byref(bs),
+    _check(api.lib().vdfcg_fit_cells_warm(_ctx(batch.axes[0], out.weights).handle, C.byref(batch.struct), C.byref(bs),
                                           C.byref(cfg), C.byref(ws) if ws is not None else None,
                                           C.byref(rs)))
     return out
@@ -207,7 +223,7 @@ def pack_cells(results: CellResults, meta: ModelMeta):
     rec = _empty(like, (max(cap, 1),), "u8")
     offs = _empty(like, (results.n_cells + 1,), "i64")
     rs = results.struct()
-    _check(api.lib().vdfcg_pack_cells(api.context().handle, results.n_cells, results.d,
+    _check(api.lib().vdfcg_pack_cells(_ctx(results.weights).handle, results.n_cells, results.d,
                                       C.byref(rs), C.byref(ms), _ptr(rec), cap, _ptr(offs)))
     total = int(offs[-1])
     return rec[:total], offs
@@ -241,7 +257,7 @@ def compress_cells(batch: CellBatch, config: FitConfig, meta: Optional[ModelMeta
         offs = _empty(like, (batch.n_cells + 1,), "i64")
     ws = warm.struct() if warm is not None else None
     _check(api.lib().vdfcg_compress_cells_warm(
-        api.context().handle, C.byref(batch.struct), C.byref(cfg),
+        _ctx(batch.axes[0], results.weights).handle, C.byref(batch.struct), C.byref(cfg),
         C.byref(ws) if ws is not None else None, C.byref(bs) if bins is not None else None,
         C.byref(rs), C.byref(ms) if ms is not None else None, _ptr(rec), cap, _ptr(offs)))
     if rec is not None:
@@ -277,7 +293,7 @@ def cell_metrics(batch: CellBatch, bins: CellBins, results: CellResults,
     api = _api()
     out = out or CellMetrics(batch.axes[0], batch.n_cells)
     bs, rs, ms = bins.struct(), results.struct(), out.struct()
-    _check(api.lib().vdfcg_metrics_cells(api.context().handle, C.byref(batch.struct), C.byref(bs),
+    _check(api.lib().vdfcg_metrics_cells(_ctx(batch.axes[0], results.weights).handle, C.byref(batch.struct), C.byref(bs),
                                          C.byref(rs), C.byref(ms)))
     return out
 
@@ -287,7 +303,7 @@ def synth_cells(d: int, cell_offsets, seed: int, species: int, u, v, w=None,
     """Deterministic synthetic plasma cells into device tensors (tests/bench data).
     cell_offsets: GLOBAL particle offsets of cells [cell_base, cell_base + n)."""
     api = _api()
-    _check(api.lib().vdfcg_synth_cells(api.context().handle, d, int(cell_offsets.shape[0]) - 1,
+    _check(api.lib().vdfcg_synth_cells(_ctx(u).handle, d, int(cell_offsets.shape[0]) - 1,
                                        _ptr(cell_offsets), int(cell_base),
                                        seed & 0xFFFFFFFFFFFFFFFF, species, _ptr(u), _ptr(v),
                                        _ptr(w)))

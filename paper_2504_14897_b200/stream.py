@@ -62,13 +62,15 @@ class RecordStream:
     def append_records(self, records, offsets, cell_base: int = 0) -> None:
         """records / offsets from compress_cells or pack_cells (host or device)."""
         n = int(offsets.shape[0]) - 1
-        _check(self._lib.vdfcg_stream_append_records(self._h, _api().context().handle,
+        from .cells import _ctx
+        _check(self._lib.vdfcg_stream_append_records(self._h, _ctx(records, offsets).handle,
                                                      _ptr(records), _ptr(offsets), n, int(cell_base)))
 
     def append_h2d(self, batch, bins, cell_base: int = 0) -> None:
         """One .h2d payload per cell of a 2V CellBatch from its CellBins."""
         bs = bins.struct()
-        _check(self._lib.vdfcg_stream_append_h2d(self._h, _api().context().handle,
+        from .cells import _ctx
+        _check(self._lib.vdfcg_stream_append_h2d(self._h, _ctx(batch.axes[0]).handle,
                                                  C.byref(batch.struct), C.byref(bs), int(cell_base)))
 
     def close(self) -> tuple[int, int]:
