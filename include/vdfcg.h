@@ -117,7 +117,12 @@ const char* vdfcg_last_error(void);
 int vdfcg_abi_version(void);
 int vdfcg_ctx_create(int device, vdfcg_ctx** out);
 int vdfcg_ctx_destroy(vdfcg_ctx* ctx);
-/* Use an external stream (e.g. torch.cuda.current_stream().cuda_stream). NULL restores the own stream. */
+/* Ordering: a call whose inputs and outputs are all device memory is asynchronous — it
+ * is enqueued on the context stream and returns; results are ready for work ordered
+ * after it on that stream (or after vdfcg_ctx_synchronize). Calls with any host buffer
+ * return after their host outputs are written. Set the context stream to the caller's
+ * stream (e.g. torch.cuda.current_stream().cuda_stream) to order library work with the
+ * caller's kernels; NULL restores the context's own stream. */
 int vdfcg_ctx_set_stream(vdfcg_ctx* ctx, void* cuda_stream);
 int vdfcg_ctx_synchronize(vdfcg_ctx* ctx);
 /* Per-kernel device timing (CUDA events on the context stream). When enabled, every
