@@ -247,6 +247,37 @@ def cpu_oracle_rate(cfg, cells_per_species, threads, gpu_results=None):
     return tot_p / tot_t, tot_f / tot_t, tot_t, tot_p, tot_f, par
 
 
+def refem_speed_check():
+    """The port is a fair stand-in for the reference: time the oracle's fit and the
+    reference's own refem::fit (proj/tests/support/reference_em.cpp, compiled from the
+    reference sources into oracle/_ref) on the same unit-weight 2D point sets, 1 thread."""
+    if ORACLE_DIR not in sys.path:
+        sys.path.insert(0, ORACLE_DIR)
+    import oracle as O
+    from paper_2504_14897_b200.types import FitConfig, WeightedPoints
+    if not O.refem_available():
+        return None
+    rng = np.random.default_rng(3)
+    sets = []
+    for i in range(6):
+        x = np.concatenate([rng.normal(size=(3000, 2)), 0.5 * rng.normal(size=(1000, 2)) + [3.0, 0.0]])
+        sets.append(x)
+    t_o = t_r = 0.0
+    pts_its = 0.0
+    for i, x in enumerate(sets):
+        t0 = time.perf_counter()
+        r = O.fit(WeightedPoints.from_(x, np.ones(len(x))), FitConfig(initial_components=4, seed=i, temperature=np.ones(2)))
+        t_o += time.perf_counter() - t0
+        t0 = time.perf_counter()
+        g = O.refem_fit(x[:, 0], x[:, 1], m=4, seed=i, temperature=(1.0, 1.0))
+        t_r += time.perf_counter() - t0
+        pts_its += len(x) * r.iterations_used
+        assert r.iterations_used == g["iterations"]
+    return {"fits": len(sets), "points_per_fit": len(sets[0]), "oracle_s": t_o, "reference_refem_s": t_r,
+            "oracle_over_reference_time": t_o / t_r,
+            "note": "unit-weight 2D fits, K=4, 1 thread: the oracle port vs the reference's own EM"}
+
+
 def compare_sample(g, o, sel, d):
     """GPU results (numpy view of a CellResults over all of this rank's cells) vs the
     oracle on the sampled cells."""
@@ -519,11 +550,16 @@ def run_gpu(args, cfg):
         runs.sort(key=lambda o: o[0])
         rate, frate, sec, sp, sf, _ = runs[len(runs) // 2]
         r1 = cpu_oracle_rate(cfg, max(1, args.cpu_cells // 16), 1)
+        try:
+            refem = refem_speed_check()
+        except Exception as e:  # the check is informational
+            refem = {"error": str(e)[:200]}
         cpu = {"value": rate, "unit": "particles/s", "cores": threads, "kind": "port",
                "fits_per_s": frate, "seconds": sec, "repeats": len(runs),
                "values_all_repeats": [o[0] for o in runs],
                "single_core_value": r1[0], "single_core_fits_per_s": r1[1],
                "single_core_sample": f"{int(r1[4])} cells ({int(r1[3])} particles), 1 thread",
+               "port_vs_reference_refem": refem,
                "sample": f"{int(sf)} cells ({int(sp)} particles) per repeat: every "
                          f"{cfg['cells'] // max(args.cpu_cells, 1)}th cell of each species, "
                          "bin+compact+fit per cell on a thread pool (oracle/ C++ restatement); "
