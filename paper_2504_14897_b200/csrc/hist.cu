@@ -17,6 +17,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include <algorithm>
+#include <string>
 
 #include "common.cuh"
 #include "hist.cuh"
@@ -933,8 +934,30 @@ static void bin_cells_d(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
     const char* e = getenv("VDFCG_HIST_TMA");  // 0: off, 1: 512-thread CTAs, 2: 256
     return e ? atoi(e) : 1;
   }();
+  // path override for measurements: VDFCG_HIST_PATH = tma | bitmap | sort | dense
+  static const int path_env = [] {
+    const char* e = getenv("VDFCG_HIST_PATH");
+    if (!e) return 0;
+    const std::string v(e);
+    return v == "tma" ? 1 : v == "bitmap" ? 2 : v == "sort" ? 3 : v == "dense" ? 4 : 0;
+  }();
   const int tb = tma_env == 2 ? 256 : 512;
-  if (!weighted && sparse && aligned && tma_env && tma_smem <= 110 * 1024 && words <= 16 * tb) {
+  const bool tma_fits = aligned && tma_env && tma_smem <= 220 * 1024 && words <= 16 * tb;
+  // Unit weights, measured on 65536 cells (tools: exp-style sweeps recorded in DESIGN.md):
+  // the TMA bitmap kernel whenever it fits two CTAs per SM (1907 particles/cell,
+  // 16^3..48^3: 0.74-1.0 ms, 6x the dense path at 16^3), or one CTA per SM with a bitmap of
+  // <= 4096 words (6000/cell, 16^3..32^3: 2.6-3.0 ms vs 6-18 ms dense); else the plain
+  // bitmap kernel for bitmaps of <= 4096 words (6000/cell at 48^3: 4.5 ms vs 11.5 sort);
+  // larger bitmaps (64^3) favour the radix sort (1907/cell: 2.0 ms vs 2.4 TMA, 7.6 bitmap).
+  const bool bitmap_fits = words * 8 + ccap * 4 + kcap * 4 <= 160 * 1024;
+  int choice = path_env;
+  if (choice == 0 && !weighted) {
+    if (tma_fits && tma_smem <= 110 * 1024) choice = 1;
+    else if (tma_fits && words <= 4096) choice = 1;
+    else if (sparse && bitmap_fits && words <= 4096) choice = 2;
+    else if (maxc <= 8192 && sparse) choice = 3;
+  }
+  if (!weighted && tma_fits && choice == 1) {
     const bool w8 = words <= 8 * tb;
     auto k = tb == 512 ? (w8 ? cells_bitmap_tma_kernel<D, 512, 8> : cells_bitmap_tma_kernel<D, 512, 16>)
                        : (w8 ? cells_bitmap_tma_kernel<D, 256, 8> : cells_bitmap_tma_kernel<D, 256, 16>);
@@ -949,7 +972,7 @@ static void bin_cells_d(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
                                                         out.nnz, out.keys, out.counts, out.oor, out.in_range));
     done = true;
   }
-  if (!done && !weighted && sparse && words * 8 + ccap * 4 + kcap * 4 <= 160 * 1024) {
+  if (!done && !weighted && bitmap_fits && (choice == 2 || (choice == 0 && sparse))) {
     const int cap = static_cast<int>(std::max<int64_t>(kcap, 1));
     const size_t smem = size_t(words) * 8 + size_t(ccap) * 4 + size_t(cap) * 4;
     auto k = cells_bitmap_kernel<D, 256>;
@@ -964,7 +987,7 @@ static void bin_cells_d(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
                                                      out.in_range));
     done = true;
   }
-  if (!done && maxc <= 8192 && (weighted || sparse)) {
+  if (!done && maxc <= 8192 && (weighted || choice == 3 || (choice == 0 && sparse))) {
     done = weighted ? try_sort_path<D, true>(ctx, c, out, g, binbits, maxc, err)
                     : try_sort_path<D, false>(ctx, c, out, g, binbits, maxc, err);
   }
