@@ -789,9 +789,19 @@ VDFCG_DEV int key_prologue(const KeyCells& kc, int c, const EmConfig& cfg, EmSta
 }
 
 template <int D, int K, bool KEYS, bool F32 = false>
-// 128 registers for K <= 4 measured best on cfg4 (112: 578 ms, 120: 555, 128: 538, 136: 637,
-// 152: 547 per species): 16 resident fits per SM with a few loop-invariant spills.
-__global__ void __launch_bounds__(256) __maxnreg__(K <= 4 ? 128 : 255) em_kernel(KeyCells kc, CoordArgs ca, EmConfig cfg,
+// Register caps measured on 48^3 cells: K = 4 at 128 (112: 578 ms, 120: 555, 128: 538,
+// 136: 637, 152: 547 per cfg4 species); K = 3 at 128 (104: 224, 112: 218, 128: 201 ms per
+// 131072 cells); K <= 2 at 80 (K=2: 72: 63.6, 80: 59.9, 88: 62.0, 128: 63.5 ms).
+#ifndef VDFCG_EM_MAXREG_K1
+#define VDFCG_EM_MAXREG_K1 80
+#endif
+#ifndef VDFCG_EM_MAXREG_K2
+#define VDFCG_EM_MAXREG_K2 80
+#endif
+#ifndef VDFCG_EM_MAXREG_K3
+#define VDFCG_EM_MAXREG_K3 128
+#endif
+__global__ void __launch_bounds__(256) __maxnreg__(K == 1 ? VDFCG_EM_MAXREG_K1 : K == 2 ? VDFCG_EM_MAXREG_K2 : K == 3 ? VDFCG_EM_MAXREG_K3 : (K <= 4 ? 128 : 255)) em_kernel(KeyCells kc, CoordArgs ca, EmConfig cfg,
                                                  EmOut out, int* counter, int red_stride) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   EmState<D, K>& S = *reinterpret_cast<EmState<D, K>*>(smem_raw);
