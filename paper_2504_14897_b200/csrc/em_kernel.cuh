@@ -791,7 +791,8 @@ VDFCG_DEV int key_prologue(const KeyCells& kc, int c, const EmConfig& cfg, EmSta
 template <int D, int K, bool KEYS, bool F32 = false>
 // Register caps measured on 48^3 cells: K = 4 at 128 (112: 578 ms, 120: 555, 128: 538,
 // 136: 637, 152: 547 per cfg4 species); K = 3 at 128 (104: 224, 112: 218, 128: 201 ms per
-// 131072 cells); K <= 2 at 80 (K=2: 72: 63.6, 80: 59.9, 88: 62.0, 128: 63.5 ms).
+// 131072 cells); K <= 2 at 80 (K=2: 72: 63.6, 80: 59.9, 88: 62.0, 128: 63.5 ms); K >= 5 at
+// 255 (K=8: 200: 337, 224: 326, 255: 240 ms per 65536 cells).
 #ifndef VDFCG_EM_MAXREG_K1
 #define VDFCG_EM_MAXREG_K1 80
 #endif
