@@ -788,7 +788,7 @@ VDFCG_DEV int key_prologue(const KeyCells& kc, int c, const EmConfig& cfg, EmSta
   return n;
 }
 
-template <int D, int K, bool KEYS, bool F32 = false>
+template <int D, int K, bool KEYS, bool F32 = false, bool CLU = false>
 // Register caps measured on 48^3 cells: K = 4 at 128 (112: 578 ms, 120: 555, 128: 538,
 // 136: 637, 152: 547 per cfg4 species); K = 3 at 128 (104: 224, 112: 218, 128: 201 ms per
 // 131072 cells); K <= 2 at 80 (K=2: 72: 63.6, 80: 59.9, 88: 62.0, 128: 63.5 ms); K >= 5 at
@@ -832,7 +832,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(K == 1 ? VDFCG_EM_MAXREG_K1 :
       __syncthreads();
       CoordSrc<D> src{ca.z, ca.n, ca.w};
       if (S.status) {
-        if (threadIdx.x == 0 && cluster_rank<!KEYS>() == 0) {
+        if (threadIdx.x == 0 && cluster_rank<CLU>() == 0) {
           out.status[c] = S.status;
           out.comps[c] = 0;
           out.iters[c] = 0;
@@ -843,7 +843,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(K == 1 ? VDFCG_EM_MAXREG_K1 :
           if (out.err_value) out.err_value[c] = S.fr.err_value;
         }
       } else {
-        run_fit<D, K, false, !KEYS>(src, static_cast<int>(ca.n), S, red, cfg, out, c);
+        run_fit<D, K, false, CLU>(src, static_cast<int>(ca.n), S, red, cfg, out, c);
       }
     }
     __syncthreads();
@@ -867,10 +867,19 @@ void launch_em_tf(vdfcg_ctx* ctx, const KeyCells& kc, const CoordArgs& ca,
   int* counter = arena<int>(ctx, 1);
   VDFCG_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), ctx->stream));
   if constexpr (!KEYS) {
-    // one fit: a cluster of CTAs, ~4 points per lane each, at most 16 (non-portable size)
+    // one fit: a cluster of CTAs, ~4 points per lane each, at most 16 (non-portable size);
+    // up to ~8 points per lane a single CTA without cluster barriers is faster (measured:
+    // 1684 points 0.47 ms alone vs 0.49 ms on two CTAs; 12.7K points 1.59 ms on 13 CTAs)
     const int64_t per_cta = int64_t(G) * 32 * 4;
-    const int cl = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(1, (ca.n + per_cta - 1) / per_cta)));
-    if (cl > 8) VDFCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    int cl = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(1, (ca.n + per_cta - 1) / per_cta)));
+    if (cl <= 2) cl = 1;
+    if (cl == 1) {
+      VDFCG_LAUNCH(ctx, "em_fit", k<<<1, G * 32, smem, ctx->stream>>>(kc, ca, cfg, out, counter, red_stride));
+      return;
+    }
+    auto kc2 = em_kernel<D, K, KEYS, F32, true>;
+    VDFCG_CUDA(cudaFuncSetAttribute(kc2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    if (cl > 8) VDFCG_CUDA(cudaFuncSetAttribute(kc2, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(cl);
     lc.blockDim = dim3(G * 32);
@@ -883,7 +892,7 @@ void launch_em_tf(vdfcg_ctx* ctx, const KeyCells& kc, const CoordArgs& ca,
     at[0].val.clusterDim.z = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
-    VDFCG_LAUNCH(ctx, "em_fit", cudaLaunchKernelEx(&lc, k, kc, ca, cfg, out, counter, red_stride));
+    VDFCG_LAUNCH(ctx, "em_fit", cudaLaunchKernelEx(&lc, kc2, kc, ca, cfg, out, counter, red_stride));
   } else {
     const int grid = std::max(1, std::min(n_cells, ctx->sm_count * occ));
     VDFCG_LAUNCH(ctx, "em_fit",
