@@ -84,6 +84,7 @@ struct KeyCells {
   uint32_t* packed;        // scratch [n_particles]: decoded bin indices (device)
   int n_bins;
   double lo[3], hi[3];
+  int cluster = 1;         // CTAs per cell (thread-block cluster) when few, large cells
 };
 
 struct CoordArgs {

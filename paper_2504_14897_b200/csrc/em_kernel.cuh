@@ -815,14 +815,16 @@ __global__ void __launch_bounds__(256) __maxnreg__(K == 1 ? VDFCG_EM_MAXREG_K1 :
   for (int pass = 0;; ++pass) {
     // cells: persistent CTAs pull fits from a queue; a single fit (!KEYS) is processed once
     // by every CTA of the cluster
-    if (KEYS && threadIdx.x == 0) S.cell = atomicAdd(counter, 1);
+    // (cells on clusters: one cell per cluster, one pass)
+    if (KEYS && !CLU && threadIdx.x == 0) S.cell = atomicAdd(counter, 1);
     __syncthreads();
-    const int c = KEYS ? S.cell : pass;
+    const int c = KEYS ? (CLU ? (pass == 0 ? static_cast<int>(blockIdx.x) / cluster_size<CLU>() : n_cells) : S.cell)
+                       : pass;
     if (c >= n_cells) break;
     if (KEYS) {
       KeySrc<D> src;
       const int n = key_prologue<D, K>(kc, c, cfg, S, ztab, red, src);
-      run_fit<D, K, F32, false>(src, n, S, red, cfg, out, c);
+      run_fit<D, K, F32, CLU>(src, n, S, red, cfg, out, c);
     } else {
       if (threadIdx.x == 0) {
         S.fr = *ca.frame;
@@ -894,6 +896,26 @@ void launch_em_tf(vdfcg_ctx* ctx, const KeyCells& kc, const CoordArgs& ca,
     lc.numAttrs = 1;
     VDFCG_LAUNCH(ctx, "em_fit", cudaLaunchKernelEx(&lc, kc2, kc, ca, cfg, out, counter, red_stride));
   } else {
+    const int cl = F32 ? 1 : std::min(16, std::max(1, kc.cluster));
+    if (cl > 1) {  // few, large cells: one cell per cluster of `cl` CTAs
+      auto kc2 = em_kernel<D, K, KEYS, F32, true>;
+      VDFCG_CUDA(cudaFuncSetAttribute(kc2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      if (cl > 8) VDFCG_CUDA(cudaFuncSetAttribute(kc2, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(n_cells * cl);
+      lc.blockDim = dim3(G * 32);
+      lc.dynamicSmemBytes = smem;
+      lc.stream = ctx->stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = cl;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      VDFCG_LAUNCH(ctx, "em_fit", cudaLaunchKernelEx(&lc, kc2, kc, ca, cfg, out, counter, red_stride));
+      return;
+    }
     const int grid = std::max(1, std::min(n_cells, ctx->sm_count * occ));
     VDFCG_LAUNCH(ctx, "em_fit",
                  k<<<grid, G * 32, smem, ctx->stream>>>(kc, ca, cfg, out, counter, red_stride));
