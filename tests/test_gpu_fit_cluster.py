@@ -46,3 +46,19 @@ def test_cluster_fit_bitwise_deterministic():
     assert a.loglik_trace == b.loglik_trace
     for x, y in zip(a.model.components, b.model.components):
         assert x.weight == y.weight and np.array_equal(x.mean, y.mean) and np.array_equal(x.covariance, y.covariance)
+
+
+def test_cluster_fit_error_path():
+    """A large point set (cluster launch) with zero spread on one axis raises the
+    reference's message, like the single-CTA path."""
+    import paper_2504_14897_b200 as G
+    from paper_2504_14897_b200.types import InvalidArgument
+    rng = np.random.default_rng(1)
+    x = rng.normal(size=(20000, 3))
+    x[:, 1] = 0.25
+    wp = WeightedPoints.from_(x, np.ones(len(x)))
+    cfg = FitConfig(initial_components=4, seed=1, temperature=np.ones(3))
+    with pytest.raises(InvalidArgument, match="axis 1 has zero spread"):
+        G.fit(wp, cfg)
+    with pytest.raises(InvalidArgument, match="axis 1 has zero spread"):
+        O.fit(wp, cfg)
