@@ -1,5 +1,7 @@
 #!/bin/bash
-# One GPU-box session producing the round's evidence into gpurun_out/ (copied to profiles/).
+# One GPU-box session producing the round's evidence into gpurun_out/ (copied to profiles/):
+#   smoke, bench (+ reference arm), ncu launch list + full capture of the bench's top
+#   kernels, single-fit latency, cell-metrics timing and the K x bins sweep.
 set -u
 OUT=gpurun_out
 mkdir -p $OUT
@@ -13,4 +15,10 @@ timeout 600 $CMD > $OUT/plain.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1
 # full capture of the two top kernels on the SAME bench command (first launch of each)
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"em_kernel|cells_bitmap|cells_sort|cells_dense" -c 2 -o $OUT/prof_round $CMD > $OUT/ncu_full.log 2>&1
+if [ "${ROUND_EXTRA:-1}" = "1" ]; then
+  timeout 300 python tools/prof_fit.py > $OUT/fit_latency.txt 2>&1
+  timeout 300 python tools/prof_metrics.py > $OUT/metrics_time.txt 2>&1
+  timeout 300 python tools/prof_metrics.py --d 2 --bins 64 --cells 65536 --per 5000 >> $OUT/metrics_time.txt 2>&1
+  timeout 1200 python tools/sweep.py --json $OUT/sweep.json > $OUT/sweep.md 2>&1
+fi
 echo done
