@@ -389,17 +389,21 @@ VDFCG_DEV void run_fit(const Src& src, int n, EmState<D, K>& S, double* red, con
         S.cst[lane] *= kLog2E;
 #pragma unroll
         for (int a = 0; a < D; ++a) S.muc[lane][a] = S.mu[lane][a];
+        if constexpr (F32) {  // single-precision copy for the FP32 E-step only
 #pragma unroll
-        for (int e = 0; e < 6; ++e) S.Af[lane][e] = static_cast<float>(S.A[lane][e]);
+          for (int e = 0; e < 6; ++e) S.Af[lane][e] = static_cast<float>(S.A[lane][e]);
 #pragma unroll
-        for (int a = 0; a < 3; ++a) S.bf[lane][a] = static_cast<float>(S.bv[lane][a]);
-        S.cstf[lane] = static_cast<float>(S.cst[lane]);
+          for (int a = 0; a < 3; ++a) S.bf[lane][a] = static_cast<float>(S.bv[lane][a]);
+          S.cstf[lane] = static_cast<float>(S.cst[lane]);
+        }
       } else if (lane < EmState<D, K>::KP) {  // inactive / padding slot: contributes zero
+        if constexpr (F32) {
 #pragma unroll
-        for (int e = 0; e < 6; ++e) S.Af[lane][e] = 0.0f;
+          for (int e = 0; e < 6; ++e) S.Af[lane][e] = 0.0f;
 #pragma unroll
-        for (int a = 0; a < 3; ++a) S.bf[lane][a] = 0.0f;
-        S.cstf[lane] = -__int_as_float(0x7f800000);
+          for (int a = 0; a < 3; ++a) S.bf[lane][a] = 0.0f;
+          S.cstf[lane] = -__int_as_float(0x7f800000);
+        }
         S.cst[lane] = -dinf();
 #pragma unroll
         for (int e = 0; e < 6; ++e) S.A[lane][e] = 0.0;
