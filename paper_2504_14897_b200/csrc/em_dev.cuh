@@ -145,10 +145,12 @@ VDFCG_DEV double exp2_nonpos(double x, const double* tab) {
   const int k = __double2loint(tm);
   const double kd = tm - kExp2C[1];
   const double r = fma(-kd, kExp2C[2], x);  // exact
-  double p = fma(r, kExp2C[3], kExp2C[4]);
-  p = fma(p, r, kExp2C[5]);
-  p = fma(p, r, kExp2C[6]);
-  p = fma(p, r, 1.0);
+  // Estrin: dependency depth 3 instead of Horner's 4 (one more FP64 op)
+  const double r2 = r * r;
+  const double lo = fma(kExp2C[6], r, 1.0);
+  double hi = fma(kExp2C[4], r, kExp2C[5]);
+  hi = fma(kExp2C[3], r2, hi);
+  const double p = fma(hi, r2, lo);
   const double v = tab[k & 255] * p;
   return __hiloint2double(__double2hiint(v) + ((k >> 8) << 20), __double2loint(v));
 }
