@@ -138,9 +138,11 @@ __device__ __constant__ double kExp2C[7] = {
 constexpr double kLog2E = 1.4426950408889634;
 constexpr double kSqrtHalfLog2E = 0.84932180028801907;  // sqrt(log2(e) / 2)
 
-// 2^x for x <= 0 (x clamped at -1021: 2^-1021 ~ 4.5e-308, below every tolerance).
+// 2^x for x <= 0; 0 below -1021 (2^-1021 ~ 4.5e-308, below every tolerance).
 VDFCG_DEV double exp2_nonpos(double x, const double* tab) {
-  x = x < -1021.0 ? -1021.0 : x;
+  // the range check runs beside the evaluation and selects 0 at the end (off the
+  // dependency chain); below -1021 (and for -inf) the evaluation itself is garbage
+  const bool tiny = x < -1021.0;
   const double tm = fma(x, kExp2C[0], kExp2C[1]);
   const int k = __double2loint(tm);
   const double kd = tm - kExp2C[1];
@@ -152,7 +154,8 @@ VDFCG_DEV double exp2_nonpos(double x, const double* tab) {
   hi = fma(kExp2C[3], r2, hi);
   const double p = fma(hi, r2, lo);
   const double v = tab[k & 255] * p;
-  return __hiloint2double(__double2hiint(v) + ((k >> 8) << 20), __double2loint(v));
+  const double out = __hiloint2double(__double2hiint(v) + ((k >> 8) << 20), __double2loint(v));
+  return tiny ? 0.0 : out;
 }
 
 // log(s) for the per-point mixture normaliser (any positive normal double; s >= 1e-300
