@@ -376,6 +376,18 @@ int vdfcg_synth_cells(vdfcg_ctx* ctx, int32_t dimension, int32_t n_cells,
                       int32_t species, double* velocity_u, double* velocity_v,
                       double* velocity_w);
 
+/* Replaces vdfc::generate (synthdata.hpp / synthdata.cpp:54-86; validation as
+ * ScenarioSpec::validate, synthdata.cpp:32-52): the reference's Gaussian-mixture particle
+ * generator drawing from the same single mt19937_64(seed) stream (rng.hpp:17-48), on the
+ * device. fractions[m], means[m*d], covs[m*d*d] (row-major per component) are host
+ * arrays; velocities (n x d column-major = SoA) is a host or device buffer;
+ * nominal_temperature[d] (host, may be null). Component choice and stream positions are
+ * bit-identical to the reference; values agree to the last few ulp (CUDA's log/sin/cos vs
+ * the host libm). Needs (n + 2*ceil(n*d/2)) * 8 bytes of device workspace. */
+int vdfcg_generate(vdfcg_ctx* ctx, int32_t dimension, int32_t m, const double* fractions,
+                   const double* means, const double* covs, int64_t n, uint64_t seed,
+                   double* velocities, double* nominal_temperature);
+
 /* Roofline denominators: FP64 and FP32 FMA throughput of this device, measured with a
  * dependent-chain-free FMA loop on every SM (TFLOP/s, FMA = 2 flops). */
 int vdfcg_probe_peaks(vdfcg_ctx* ctx, double* fp64_tflops, double* fp32_tflops);

@@ -61,6 +61,7 @@ def _bind(lib) -> None:
         "vdfcg_compress_cells_warm": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, i64, vp]),
         "vdfcg_synth_cells": (C.c_int, [vp, i32, i32, vp, i64, u64, i32, vp, vp, vp]),
         "vdfcg_probe_peaks": (C.c_int, [vp, vp, vp]),
+        "vdfcg_generate": (C.c_int, [vp, i32, i32, vp, vp, vp, i64, u64, vp, vp]),
         "vdfcg_metrics_cells": (C.c_int, [vp, vp, vp, vp, vp]),
         "vdfcg_evaluate_pdf": (C.c_int, [vp, vp, i32, f64, f64, f64, f64, vp]),
         "vdfcg_weighted_loglik": (C.c_int, [vp, vp, vp, vp, i64, vp]),
@@ -212,6 +213,32 @@ def probe_peaks() -> tuple[float, float]:
     f64, f32 = C.c_double(0.0), C.c_double(0.0)
     _marshal.check(lib().vdfcg_probe_peaks(context().handle, C.byref(f64), C.byref(f32)), last_error)
     return f64.value, f32.value
+
+
+def generate(fractions, means, covs, n: int, seed: int, label: str = "synthetic",
+             out=None) -> ParticleSet:
+    """synthdata.cpp:54-86 generate(ScenarioSpec) on the device: the reference's mixture
+    generator on its own mt19937_64(seed) stream. ``out`` may be a CUDA tensor of n*d
+    float64 (column-major velocities are written there and the returned ParticleSet holds
+    a host copy only when ``out`` is None)."""
+    means = np.asarray(means, dtype=np.float64)
+    covs = np.asarray(covs, dtype=np.float64)
+    m, d = means.shape
+    fr = np.ascontiguousarray(fractions, dtype=np.float64)
+    if fr.shape != (m,) or covs.shape != (m, d, d):
+        raise InvalidArgument("generate: fractions/means/covariances shape mismatch")
+    mu = np.ascontiguousarray(means.reshape(-1))
+    cv = np.ascontiguousarray(covs.reshape(-1))
+    temp = np.zeros(d)
+    if out is None:
+        vel = np.zeros((n, d), order="F")
+        ptr = vel.ctypes.data
+    else:
+        vel, ptr = out, out.data_ptr()
+    _marshal.check(lib().vdfcg_generate(context().handle, d, m, fr.ctypes.data, mu.ctypes.data,
+                                        cv.ctypes.data, n, seed & 0xFFFFFFFFFFFFFFFF, ptr,
+                                        temp.ctypes.data), last_error)
+    return ParticleSet(velocities=vel, species_label=label, nominal_temperature=temp)
 
 
 def validate_fit_config(config: FitConfig, d: int) -> None:

@@ -20,6 +20,8 @@
 namespace vdfcg {
 void launch_synth(vdfcg_ctx* ctx, int d, int n_cells, const int64_t* offsets, int64_t cell_base,
                   uint64_t seed, int species, double* u, double* v, double* w);
+void launch_generate(vdfcg_ctx* ctx, int d, int m, int64_t n, uint64_t seed, double* uniforms,
+                     int64_t n_uniforms, const double* params, double* vel);
 double probe_fp64(vdfcg_ctx* ctx);
 double probe_fp32(vdfcg_ctx* ctx);
 
@@ -1278,6 +1280,78 @@ int vdfcg_synth_cells(vdfcg_ctx* ctx, int32_t d, int32_t n_cells, const int64_t*
         (d == 3 && !is_device_pointer(w)))
       throw InvalidArgument("vdfcg_synth_cells takes device pointers");
     if (n_cells > 0) launch_synth(ctx, d, n_cells, cell_offsets, cell_base, seed, species, u, v, w);
+  });
+}
+
+// synthdata.cpp:54-86 (generate) after ScenarioSpec::validate (synthdata.cpp:32-52). The
+// scenario (m fractions, means, covariances) is host parameter data: it is validated and
+// factorised here exactly as the reference does before its particle loop; every particle
+// is drawn on the device.
+int vdfcg_generate(vdfcg_ctx* ctx, int32_t d, int32_t m, const double* fractions,
+                   const double* means, const double* covs, int64_t n, uint64_t seed,
+                   double* velocities, double* nominal_temperature) {
+  return guard_impl([&] {
+    begin(ctx);
+    if (d != 2 && d != 3) throw InvalidArgument("scenario dimension must be 2 or 3");
+    if (n < 1) throw InvalidArgument("particle_count must be >= 1");
+    if (m < 1) throw InvalidArgument("scenario needs at least one component");
+    if (!fractions || !means || !covs || !velocities) throw InvalidArgument("null argument");
+    // params: cdf[m], mean[m][d], chol[m][3][3]
+    std::vector<double> par(size_t(m) * (1 + d + 9), 0.0);
+    double total = 0.0, acc = 0.0;
+    for (int k = 0; k < m; ++k) {
+      const std::string who = "component " + std::to_string(k);
+      if (!(fractions[k] >= 0.0)) throw InvalidArgument(who + ": fraction must be >= 0");
+      const double* c = covs + size_t(k) * d * d;
+      double diff = 0.0, norm = 0.0;  // Eigen isApprox(transpose, 1e-12), Frobenius
+      for (int a = 0; a < d; ++a)
+        for (int b = 0; b < d; ++b) {
+          const double e = c[a * d + b] - c[b * d + a];
+          diff += e * e;
+          norm += c[a * d + b] * c[a * d + b];
+        }
+      if (!(diff <= 1e-24 * norm)) throw InvalidArgument(who + ": covariance is not symmetric");
+      double* L = par.data() + m + size_t(m) * d + size_t(k) * 9;  // Eigen LLT, lower
+      for (int j = 0; j < d; ++j) {
+        double x = c[j * d + j];
+        if (j > 0) {
+          double sq = 0.0;
+          for (int i = 0; i < j; ++i) sq += L[j * 3 + i] * L[j * 3 + i];
+          x -= sq;
+        }
+        const double sj = std::sqrt(x);
+        if (!(x > 0.0) || !std::isfinite(sj))
+          throw InvalidArgument(who + ": covariance is not symmetric positive definite");
+        L[j * 3 + j] = sj;
+        for (int i = j + 1; i < d; ++i) {
+          double v = c[i * d + j];
+          for (int q = 0; q < j; ++q) v -= L[i * 3 + q] * L[j * 3 + q];
+          L[i * 3 + j] = v / sj;
+        }
+      }
+      for (int a = 0; a < d; ++a) par[m + size_t(k) * d + a] = means[size_t(k) * d + a];
+      total += fractions[k];
+      acc += fractions[k];
+      par[k] = acc;
+    }
+    if (std::abs(total - 1.0) > 1e-12)
+      throw InvalidArgument("fractions must sum to 1 (got " + std::to_string(total) + ")");
+    par[m - 1] = 1.0;  // the last component owns the tail (synthdata.cpp:64)
+    if (nominal_temperature) {  // synthdata.cpp:71-73
+      for (int a = 0; a < d; ++a) nominal_temperature[a] = 0.0;
+      for (int k = 0; k < m; ++k)
+        for (int a = 0; a < d; ++a)
+          nominal_temperature[a] += fractions[k] * covs[(size_t(k) * d + a) * d + a];
+    }
+    const int64_t n_uniforms = n + 2 * ((n * d + 1) / 2);
+    double* dpar = arena<double>(ctx, par.size());
+    VDFCG_CUDA(cudaMemcpyAsync(dpar, par.data(), par.size() * sizeof(double),
+                               cudaMemcpyHostToDevice, ctx->stream));
+    double* uni = arena<double>(ctx, size_t(n_uniforms));
+    auto v = stage_out(ctx, velocities, size_t(n) * d);
+    launch_generate(ctx, d, m, n, seed, uni, n_uniforms, dpar, v.dev);
+    finish(ctx, v);
+    sync(ctx);
   });
 }
 

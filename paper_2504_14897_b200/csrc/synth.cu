@@ -73,6 +73,99 @@ void launch_synth(vdfcg_ctx* ctx, int d, int n_cells, const int64_t* offsets, in
                                                                         seed, species, u, v, w));
 }
 
+// ---------------------------------------------------------------- reference generator
+// synthdata.cpp:54-86 on the device, drawing from the reference's own stream (rng.hpp:17-48):
+// ONE mt19937_64(seed); uniform() = (x >> 11)·2⁻⁵³; normal() = Box-Muller that returns
+// r·cos and keeps r·sin as the spare for the next call. Per particle: one selection
+// uniform, then d normals. The engine is sequential, so a single CTA produces the uniform
+// stream: the in-place 312-word twist splits into two data-parallel halves (i < 156 reads
+// only untouched words; i >= 156 reads the words the first half just wrote, and i = 311
+// reads the new word 0, exactly as the sequential loop does). The transform is one thread
+// per particle at a closed-form stream offset, so it is embarrassingly parallel.
+constexpr int kMtN = 312, kMtM = 156;
+
+VDFCG_DEV uint64_t mt_twist(uint64_t upper_src, uint64_t lower_src) {
+  const uint64_t xx = (upper_src & 0xFFFFFFFF80000000ULL) | (lower_src & 0x7FFFFFFFULL);
+  return (xx >> 1) ^ ((xx & 1ULL) ? 0xB5026F5AA96619E9ULL : 0ULL);
+}
+
+VDFCG_DEV double mt_uniform(uint64_t y) {
+  y ^= (y >> 29) & 0x5555555555555555ULL;
+  y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+  y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+  y ^= (y >> 43);
+  return static_cast<double>(y >> 11) * 0x1.0p-53;
+}
+
+__global__ void __launch_bounds__(kMtM) mt_stream_kernel(uint64_t seed, int64_t count,
+                                                        double* __restrict__ out) {
+  __shared__ uint64_t mt[kMtN];
+  const int t = threadIdx.x;
+  if (t == 0) {
+    mt[0] = seed;
+    for (int i = 1; i < kMtN; ++i) mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + i;
+  }
+  __syncthreads();
+  for (int64_t base = 0; base < count; base += kMtN) {
+    // first half, i = t: mt[t + 1] and mt[t + 156] are still the previous block's words
+    const uint64_t a = mt[t + kMtM] ^ mt_twist(mt[t], mt[t + 1]);
+    const uint64_t hi_old = mt[t + kMtM];
+    __syncthreads();
+    mt[t] = a;
+    __syncthreads();
+    // second half, i = t + 156: mt[i - 156] is new; mt[i + 1] is old except mt[0] (i = 311)
+    const int i = t + kMtM;
+    const uint64_t b = mt[t] ^ mt_twist(hi_old, mt[i + 1 < kMtN ? i + 1 : 0]);
+    __syncthreads();
+    mt[i] = b;
+    if (base + t < count) out[base + t] = mt_uniform(a);
+    if (base + i < count) out[base + i] = mt_uniform(b);
+    __syncthreads();
+  }
+}
+
+// Stream offsets (normal call j = n·d + a pairs up as q = j/2; pair q is opened by the
+// particle floor(2q/d) after its selection uniform): selection uniform of particle n at
+// n + 2·ceil(n·d/2); pair q's two uniforms at floor(2q/d) + 1 + 2q.
+__global__ void generate_kernel(int d, int m, int64_t n, const double* __restrict__ uni,
+                                const double* __restrict__ par, double* __restrict__ vel) {
+  // par: cdf[m], mean[m][d], chol[m][3][3] (row-major lower factor)
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j0 = r * d;
+    const double u = uni[r + 2 * ((j0 + 1) >> 1)];
+    int k = 0;
+    while (k + 1 < m && u >= par[k]) ++k;
+    double z[3] = {0.0, 0.0, 0.0};
+    for (int a = 0; a < d; ++a) {
+      const int64_t j = j0 + a, q = j >> 1;
+      const int64_t pos = (2 * q) / d + 1 + 2 * q;
+      const double u1 = 1.0 - uni[pos];
+      const double u2 = uni[pos + 1];
+      const double rad = sqrt(-2.0 * log(u1));
+      const double ang = 6.283185307179586 * u2;  // 2.0 * M_PI * u2 (2·π folds exactly)
+      z[a] = (j & 1) ? rad * sin(ang) : rad * cos(ang);
+    }
+    const double* mean = par + m + k * d;
+    const double* L = par + m + m * d + k * 9;
+    for (int a = 0; a < d; ++a) {
+      double s = 0.0;  // no FMA contraction: the reference builds without -march
+      for (int b = 0; b < d; ++b) s = __dadd_rn(s, __dmul_rn(L[a * 3 + b], z[b]));
+      vel[static_cast<int64_t>(a) * n + r] = __dadd_rn(mean[a], s);
+    }
+  }
+}
+
+void launch_generate(vdfcg_ctx* ctx, int d, int m, int64_t n, uint64_t seed, double* uniforms,
+                     int64_t n_uniforms, const double* params, double* vel) {
+  VDFCG_LAUNCH(ctx, "mt19937_64_stream",
+               mt_stream_kernel<<<1, kMtM, 0, ctx->stream>>>(seed, n_uniforms, uniforms));
+  const int grid = static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>((n + 255) / 256, static_cast<int64_t>(ctx->sm_count) * 16)));
+  VDFCG_LAUNCH(ctx, "generate",
+               generate_kernel<<<grid, 256, 0, ctx->stream>>>(d, m, n, uniforms, params, vel));
+}
+
 // ---------------------------------------------------------------- peak probe
 // 8 independent FMA chains per thread, 64K iterations: issue-bound FMA throughput.
 template <class T>
