@@ -538,7 +538,7 @@ Model m_step_impl(const Points& p, double total, const std::vector<double>& resp
     for (int a = 0; a < d; ++a)
       for (int b = 0; b < d; ++b) finite = finite && std::isfinite(sigma[a][b]);
     if (finite) {
-      double ev[3];
+      double ev[3] = {0.0, 0.0, 0.0};
       sym_eigenvalues(sigma, d, ev);
       double mn = ev[0], mx = ev[0];
       for (int a = 1; a < d; ++a) {
