@@ -20,7 +20,7 @@
 namespace vdfcg {
 void launch_synth(vdfcg_ctx* ctx, int d, int n_cells, const int64_t* offsets, int64_t cell_base,
                   uint64_t seed, int species, double* u, double* v, double* w);
-void launch_generate(vdfcg_ctx* ctx, int d, int m, int64_t n, uint64_t seed, double* uniforms,
+void launch_generate(vdfcg_ctx* ctx, int d, int m, int64_t n, uint64_t seed, uint64_t* uniforms,
                      int64_t n_uniforms, const double* params, double* vel);
 double probe_fp64(vdfcg_ctx* ctx);
 double probe_fp32(vdfcg_ctx* ctx);
@@ -1347,7 +1347,7 @@ int vdfcg_generate(vdfcg_ctx* ctx, int32_t d, int32_t m, const double* fractions
     double* dpar = arena<double>(ctx, par.size());
     VDFCG_CUDA(cudaMemcpyAsync(dpar, par.data(), par.size() * sizeof(double),
                                cudaMemcpyHostToDevice, ctx->stream));
-    double* uni = arena<double>(ctx, size_t(n_uniforms));
+    uint64_t* uni = arena<uint64_t>(ctx, size_t(n_uniforms));  // raw mt19937_64 words
     auto v = stage_out(ctx, velocities, size_t(n) * d);
     launch_generate(ctx, d, m, n, seed, uni, n_uniforms, dpar, v.dev);
     finish(ctx, v);

@@ -97,51 +97,66 @@ VDFCG_DEV double mt_uniform(uint64_t y) {
   return static_cast<double>(y >> 11) * 0x1.0p-53;
 }
 
+// Thread t < 156 keeps the pair (mt[t], mt[t + 156]) in registers. The sequential twist
+// gives  mt'[t] = mt[t+156] ^ T(mt[t], mt[t+1])  and  mt'[t+156] = mt'[t] ^ T(mt[t+156],
+// mt[t+157]), where mt[312] means the NEW word 0 (the loop wraps after updating it), so a
+// thread needs only its right neighbour's old pair: one double-buffered shared-memory
+// exchange and ONE barrier per 312 words. Thread 155 recomputes the new word 0 itself.
+// The single CTA stores the raw (untempered) words; tempering and the 53-bit conversion run
+// in the all-SM transform, which keeps the serial kernel to the twist itself.
 __global__ void __launch_bounds__(kMtM) mt_stream_kernel(uint64_t seed, int64_t count,
-                                                        double* __restrict__ out) {
-  __shared__ uint64_t mt[kMtN];
+                                                        uint64_t* __restrict__ out) {
+  __shared__ uint64_t sh[2][2][kMtM];  // [buffer][low half / high half][t]
   const int t = threadIdx.x;
-  if (t == 0) {
-    mt[0] = seed;
-    for (int i = 1; i < kMtN; ++i) mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + i;
+  if (t == 0) {  // std::mersenne_twister_engine seeding, into buffer 1 (read on block 0)
+    uint64_t x = seed;
+    sh[1][0][0] = x;
+    for (int i = 1; i < kMtN; ++i) {
+      x = 6364136223846793005ULL * (x ^ (x >> 62)) + i;
+      sh[1][i / kMtM][i % kMtM] = x;
+    }
   }
   __syncthreads();
+  uint64_t A = sh[1][0][t], B = sh[1][1][t];
+  int p = 0;
   for (int64_t base = 0; base < count; base += kMtN) {
-    // first half, i = t: mt[t + 1] and mt[t + 156] are still the previous block's words
-    const uint64_t a = mt[t + kMtM] ^ mt_twist(mt[t], mt[t + 1]);
-    const uint64_t hi_old = mt[t + kMtM];
+    sh[p][0][t] = A;
+    sh[p][1][t] = B;
     __syncthreads();
-    mt[t] = a;
-    __syncthreads();
-    // second half, i = t + 156: mt[i - 156] is new; mt[i + 1] is old except mt[0] (i = 311)
-    const int i = t + kMtM;
-    const uint64_t b = mt[t] ^ mt_twist(hi_old, mt[i + 1 < kMtN ? i + 1 : 0]);
-    __syncthreads();
-    mt[i] = b;
-    if (base + t < count) out[base + t] = mt_uniform(a);
-    if (base + i < count) out[base + i] = mt_uniform(b);
-    __syncthreads();
+    uint64_t A1, B1;
+    if (t + 1 < kMtM) {
+      A1 = sh[p][0][t + 1];
+      B1 = sh[p][1][t + 1];
+    } else {
+      A1 = sh[p][1][0];                                        // mt[156]
+      B1 = sh[p][1][0] ^ mt_twist(sh[p][0][0], sh[p][0][1]);   // new mt[0]
+    }
+    A = B ^ mt_twist(A, A1);
+    B = A ^ mt_twist(B, B1);
+    if (base + t < count) out[base + t] = A;
+    if (base + t + kMtM < count) out[base + t + kMtM] = B;
+    p ^= 1;
   }
 }
 
 // Stream offsets (normal call j = n·d + a pairs up as q = j/2; pair q is opened by the
 // particle floor(2q/d) after its selection uniform): selection uniform of particle n at
 // n + 2·ceil(n·d/2); pair q's two uniforms at floor(2q/d) + 1 + 2q.
-__global__ void generate_kernel(int d, int m, int64_t n, const double* __restrict__ uni,
+__global__ void generate_kernel(int d, int m, int64_t n, const uint64_t* __restrict__ uni,
                                 const double* __restrict__ par, double* __restrict__ vel) {
   // par: cdf[m], mean[m][d], chol[m][3][3] (row-major lower factor)
   for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t j0 = r * d;
-    const double u = uni[r + 2 * ((j0 + 1) >> 1)];
+    const double u = mt_uniform(uni[r + 2 * ((j0 + 1) >> 1)]);
     int k = 0;
     while (k + 1 < m && u >= par[k]) ++k;
     double z[3] = {0.0, 0.0, 0.0};
     for (int a = 0; a < d; ++a) {
       const int64_t j = j0 + a, q = j >> 1;
       const int64_t pos = (2 * q) / d + 1 + 2 * q;
-      const double u1 = 1.0 - uni[pos];
-      const double u2 = uni[pos + 1];
+      const double u1 = 1.0 - mt_uniform(uni[pos]);
+      const double u2 = mt_uniform(uni[pos + 1]);
       const double rad = sqrt(-2.0 * log(u1));
       const double ang = 6.283185307179586 * u2;  // 2.0 * M_PI * u2 (2·π folds exactly)
       z[a] = (j & 1) ? rad * sin(ang) : rad * cos(ang);
@@ -156,7 +171,7 @@ __global__ void generate_kernel(int d, int m, int64_t n, const double* __restric
   }
 }
 
-void launch_generate(vdfcg_ctx* ctx, int d, int m, int64_t n, uint64_t seed, double* uniforms,
+void launch_generate(vdfcg_ctx* ctx, int d, int m, int64_t n, uint64_t seed, uint64_t* uniforms,
                      int64_t n_uniforms, const double* params, double* vel) {
   VDFCG_LAUNCH(ctx, "mt19937_64_stream",
                mt_stream_kernel<<<1, kMtM, 0, ctx->stream>>>(seed, n_uniforms, uniforms));
