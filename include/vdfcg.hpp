@@ -118,6 +118,20 @@ inline double bin_particles(const double* velocities, int64_t n, int d, const do
   return oor;
 }
 
+// vdfc::generate (synthdata.cpp:54-86): n x d column-major velocities drawn on the device
+// from the reference's mt19937_64(seed) stream; returns the nominal temperature per axis.
+inline std::vector<double> generate(int d, const std::vector<double>& fractions,
+                                    const std::vector<double>& means,
+                                    const std::vector<double>& covariances, int64_t n,
+                                    uint64_t seed, double* velocities,
+                                    Context& ctx = Context::thread_default()) {
+  std::vector<double> temperature(static_cast<size_t>(d > 0 ? d : 0));
+  check(vdfcg_generate(ctx.get(), d, static_cast<int32_t>(fractions.size()), fractions.data(),
+                       means.data(), covariances.data(), n, seed, velocities,
+                       temperature.data()));
+  return temperature;
+}
+
 // vdfc::encode_model (codec.hpp:48).
 inline std::vector<uint8_t> encode_model(const vdfcg_model& model, const vdfcg_model_meta& meta,
                                          Context& ctx = Context::thread_default()) {

@@ -83,6 +83,15 @@ int main() {
     vdfcg::check(vdfcg_stream_append_records(s, ctx.get(), rec.data(), roff.data(), nc, 0));
     int64_t n_rec = 0, n_bytes = 0;
     vdfcg::check(vdfcg_stream_close(s, &n_rec, &n_bytes));
+    std::vector<double> gv(2 * 1000);  // vdfc::generate on the device
+    const auto temp = vdfcg::generate(2, {0.8, 0.2}, {0, 0, 3, 0}, {1, 0, 0, 1, 0.25, 0, 0, 0.25},
+                                      1000, 11, gv.data());
+    std::printf("generate T=(%.3f,%.3f)\n", temp[0], temp[1]);
+    try {
+      vdfcg::generate(2, {0.5, 0.4}, {0, 0, 1, 1}, {1, 0, 0, 1, 1, 0, 0, 1}, 10, 1, gv.data());
+    } catch (const std::invalid_argument& e) {
+      std::printf("invalid_argument: %s\n", e.what());
+    }
     int ok = 0;
     for (int c = 0; c < nc; ++c) ok += st[c] == 0 && jsd[c] >= 0 && jsd[c] <= std::log(2.0) && std::isfinite(bic[c]);
     std::printf("cells ok=%d records=%lld bytes=%lld\n", ok, (long long)n_rec, (long long)n_bytes);

@@ -26,3 +26,5 @@ def test_shim_runs_on_gpu(tmp_path):
     assert r.returncode == 0, r.stdout + r.stderr
     assert "invalid_argument: fit: degenerate data: axis 0 has zero spread" in r.stdout
     assert "cells ok=64 records=64" in r.stdout
+    assert "generate T=(0.850,0.850)" in r.stdout
+    assert "invalid_argument: fractions must sum to 1" in r.stdout
