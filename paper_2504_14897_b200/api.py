@@ -234,6 +234,10 @@ def generate(fractions, means, covs, n: int, seed: int, label: str = "synthetic"
         vel = np.zeros((n, d), order="F")
         ptr = vel.ctypes.data
     else:
+        import torch
+        if (not isinstance(out, torch.Tensor) or out.dtype != torch.float64
+                or not out.is_contiguous() or out.numel() < n * d):
+            raise InvalidArgument("generate: out must be a contiguous float64 tensor of n*d values")
         vel, ptr = out, out.data_ptr()
     _marshal.check(lib().vdfcg_generate(context().handle, d, m, fr.ctypes.data, mu.ctypes.data,
                                         cv.ctypes.data, n, seed & 0xFFFFFFFFFFFFFFFF, ptr,
