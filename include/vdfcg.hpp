@@ -125,7 +125,18 @@ inline std::vector<double> generate(int d, const std::vector<double>& fractions,
                                     const std::vector<double>& covariances, int64_t n,
                                     uint64_t seed, double* velocities,
                                     Context& ctx = Context::thread_default()) {
-  std::vector<double> temperature(static_cast<size_t>(d > 0 ? d : 0));
+  // ScenarioSpec::validate's shape checks (synthdata.cpp:39-43), before any pointer is read
+  const size_t m = fractions.size(), dd = static_cast<size_t>(d > 0 ? d : 0);
+  for (size_t k = 0; k < m; ++k) {
+    const std::string who = "component " + std::to_string(k);
+    if (means.size() < (k + 1) * dd) throw std::invalid_argument(who + ": mean dimension mismatch");
+    if (covariances.size() < (k + 1) * dd * dd)
+      throw std::invalid_argument(who + ": covariance shape mismatch");
+  }
+  if (means.size() != m * dd) throw std::invalid_argument("generate: means size != m*d");
+  if (covariances.size() != m * dd * dd)
+    throw std::invalid_argument("generate: covariances size != m*d*d");
+  std::vector<double> temperature(dd);
   check(vdfcg_generate(ctx.get(), d, static_cast<int32_t>(fractions.size()), fractions.data(),
                        means.data(), covariances.data(), n, seed, velocities,
                        temperature.data()));

@@ -1,6 +1,6 @@
 """ctypes mirror of include/vdfcg.h (structs and converters only — no compute).
 
-Shared by the product wrapper (``_native.py``, which loads libvdfcg.so) and by the
+Shared by the product wrapper (``api.py``, which loads libvdfcg.so) and by the
 test-only oracle wrapper (``oracle/oracle.py``), so both sides are fed identical
 buffers.
 """

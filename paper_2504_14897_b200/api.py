@@ -233,13 +233,20 @@ def generate(fractions, means, covs, n: int, seed: int, label: str = "synthetic"
     if out is None:
         vel = np.zeros((n, d), order="F")
         ptr = vel.ctypes.data
+        ctx = context()
     else:
         import torch
-        if (not isinstance(out, torch.Tensor) or out.dtype != torch.float64
-                or not out.is_contiguous() or out.numel() < n * d):
-            raise InvalidArgument("generate: out must be a contiguous float64 tensor of n*d values")
-        vel, ptr = out, out.data_ptr()
-    _marshal.check(lib().vdfcg_generate(context().handle, d, m, fr.ctypes.data, mu.ctypes.data,
+        from .cells import _ctx
+        # column-major n x d: a flat tensor of n*d values, or an (n, d) view with stride (1, n)
+        ok = (isinstance(out, torch.Tensor) and out.dtype == torch.float64 and out.is_cuda
+              and ((out.dim() == 1 and out.numel() == n * d and out.stride(0) == 1)
+                   or (out.dim() == 2 and tuple(out.shape) == (n, d) and out.stride() == (1, n))))
+        if not ok:
+            raise InvalidArgument("generate: out must be a CUDA float64 tensor of n*d values "
+                                  "(flat, or an (n, d) column-major view with stride (1, n))")
+        ctx = _ctx(out)  # out's device, ordered on its current torch stream
+        vel, ptr = out.view(d, n).t() if out.dim() == 1 else out, out.data_ptr()
+    _marshal.check(lib().vdfcg_generate(ctx.handle, d, m, fr.ctypes.data, mu.ctypes.data,
                                         cv.ctypes.data, n, seed & 0xFFFFFFFFFFFFFFFF, ptr,
                                         temp.ctypes.data), last_error)
     return ParticleSet(velocities=vel, species_label=label, nominal_temperature=temp)

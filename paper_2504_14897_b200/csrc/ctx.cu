@@ -180,6 +180,7 @@ int vdfcg_ctx_destroy(vdfcg_ctx* ctx) {
       cudaStreamDestroy(ctx->copy_stream);
     }
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    if (ctx->handoff) cudaEventDestroy(ctx->handoff);
     delete ctx;
   });
 }
@@ -187,7 +188,16 @@ int vdfcg_ctx_destroy(vdfcg_ctx* ctx) {
 int vdfcg_ctx_set_stream(vdfcg_ctx* ctx, void* s) {
   return guard_impl([&] {
     if (!ctx) throw InvalidArgument("null context");
-    ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own_stream;
+    cudaStream_t next = s ? static_cast<cudaStream_t>(s) : ctx->own_stream;
+    if (next != ctx->stream) {
+      // Every call resets the shared arena; asynchronous work still queued on the old
+      // stream may be using it, so the new stream waits for everything enqueued so far.
+      VDFCG_CUDA(cudaSetDevice(ctx->device));
+      if (!ctx->handoff) VDFCG_CUDA(cudaEventCreateWithFlags(&ctx->handoff, cudaEventDisableTiming));
+      VDFCG_CUDA(cudaEventRecord(ctx->handoff, ctx->stream));
+      VDFCG_CUDA(cudaStreamWaitEvent(next, ctx->handoff, 0));
+      ctx->stream = next;
+    }
   });
 }
 

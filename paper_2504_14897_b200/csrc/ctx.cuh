@@ -45,6 +45,7 @@ struct vdfcg_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // H2D of later cell chunks overlaps compute
   cudaStream_t aux_stream = nullptr;   // second compute stream: chunk kernels overlap tails
+  cudaEvent_t handoff = nullptr;       // orders the arena's last user before a new stream
   // grow-only arena, reset at the start of every API call
   struct Chunk {
     char* base;

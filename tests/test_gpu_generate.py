@@ -51,6 +51,15 @@ def test_generate_device_output_and_single_component():
     o = O.generate([1.0], [[0.5, -0.25]], [[[1.0, 0.2], [0.2, 0.8]]], n, 5)
     got = out.cpu().numpy().reshape(2, n).T
     assert (np.abs(got - o.velocities) / (1.0 + np.abs(o.velocities))).max() <= TOL
+    # an (n, d) column-major view is accepted; the returned set is a usable n x d ParticleSet
+    col = torch.empty(2, n, dtype=torch.float64, device="cuda").t()
+    ps = G.generate([1.0], [[0.5, -0.25]], [[[1.0, 0.2], [0.2, 0.8]]], n, 5, out=col)
+    assert ps.count() == n and ps.dimension() == 2
+    assert torch.equal(col.cpu(), torch.from_numpy(got.copy()))
+    # row-major (n, d) would be scrambled by the column-major kernel: rejected
+    with pytest.raises(InvalidArgument, match="column-major"):
+        G.generate([1.0], [[0.5, -0.25]], [[[1.0, 0.2], [0.2, 0.8]]], n, 5,
+                   out=torch.empty(n, 2, dtype=torch.float64, device="cuda"))
 
 
 def test_generate_validation_messages():  # synthdata.cpp:32-52

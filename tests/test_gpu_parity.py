@@ -114,7 +114,7 @@ def test_encode_model_hex_vector():
                                     np.array([[1, 0.125], [0.125, 2.0]]))], AffineMap.identity(2), 2)
     b = G.encode_model(m, ModelMeta("e", Plane.uv, 50, [AxisRange(-5, 5), AxisRange(-5, 5)]))
     assert len(b) == 107
-    assert b[0x37:0x3b].hex() == "65525af6"[2:] + "5af6d7"[0:0] or True
+    assert b[55:59].hex() == "525af6d7"  # header CRC-32, FORMATS.md:35-47
     assert b == O.encode_model(m, ModelMeta("e", Plane.uv, 50, [AxisRange(-5, 5), AxisRange(-5, 5)]))
 
 

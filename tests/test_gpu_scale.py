@@ -272,3 +272,43 @@ def test_pipelined_host_path_weighted_bitwise():
     for f in ("status", "components", "iterations"):
         assert torch.equal(getattr(rd, f).cpu(), getattr(rh, f)), f
     assert torch.equal(rd.weights.cpu().view(torch.int64), rh.weights.view(torch.int64))
+
+
+def test_cfg3_full_size_parity():
+    """BASELINE cfg3 at full size: 16x16 cells x 390625 particles (1e8), 3V 32^3 bins, K=3
+    (the reference's per-part fit_one_plane, pipeline.cpp:130-160, on every cell). Every
+    cell's compacted histogram bit-exact vs the oracle; identical iterations and M-hat;
+    parameters and final log-likelihood within 1e-9 on every cell."""
+    import torch
+    dev = torch.device("cuda", 0)
+    n_cells, per = 256, 390_625
+    offs = torch.arange(n_cells + 1, dtype=torch.int64, device=dev) * per
+    axes = [torch.empty(n_cells * per, dtype=torch.float64, device=dev) for _ in range(3)]
+    G.synth_cells(3, offs, 11, 0, *axes)
+    cfg = FitConfig(initial_components=3, seed=11, temperature=np.ones(3))
+    gb, gr, _, _ = G.compress_cells(G.CellBatch(axes, offs, 32, [-6] * 3, [6] * 3), cfg)
+    offs_h = offs.cpu().numpy()
+    v = np.empty((n_cells * per, 3), order="F")
+    for a in range(3):
+        v[:, a] = axes[a].cpu().numpy()
+    del axes
+    ob, orr = O.compress_cells(O.CellsHost(v, offs_h, 32, [-6] * 3, [6] * 3), cfg,
+                               threads=os.cpu_count() or 1)
+    nnz = gb.nnz.cpu().numpy()
+    assert np.array_equal(nnz, ob.nnz)
+    keys, counts = gb.keys.cpu().numpy(), gb.counts.cpu().numpy()
+    for c in range(n_cells):
+        b, k = offs_h[c], nnz[c]
+        assert np.array_equal(keys[b:b + k], ob.keys[b:b + k]), c
+        assert np.array_equal(counts[b:b + k], ob.counts[b:b + k]), c
+    assert np.array_equal(gb.out_of_range.cpu().numpy(), ob.out_of_range)
+    assert (gr.status.cpu().numpy() == 0).all()
+    assert np.array_equal(gr.iterations.cpu().numpy(), orr.iterations)
+    assert np.array_equal(gr.components.cpu().numpy(), orr.components)
+    gres = gr.numpy()
+    worst = 0.0
+    for c in range(n_cells):
+        worst = max(worst, model_close(gres.model(c), _oracle_model(orr, c, 3)))
+    assert worst <= TOL_EM, worst
+    fl = gr.final_loglik.cpu().numpy()
+    assert _rel(fl, orr.final_loglik) <= TOL_EM
