@@ -354,6 +354,73 @@ def em_flops(res_np, nnz, K, d):
     return float(F_D[d] * np.sum(np.where(ok, nnz * comp_its, 0.0)))
 
 
+def run_indexed_leg(args, cfg, batches, fcs, metas, results, ctx, stream, dev, hbm_peak, world,
+                    barrier):
+    """The cell-index entry point on a random permutation of this rank's particles."""
+    import torch
+    from paper_2504_14897_b200.cells import ParticleBatch, compress_cells_indexed
+    d = cfg["d"]
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(SEED)
+    pbs = []
+    for b in batches:
+        perm = torch.randperm(b.n, device=dev, generator=gen)
+        cnt = (b.offsets[1:] - b.offsets[:-1]).to(torch.int64)
+        cid = torch.repeat_interleave(torch.arange(b.n_cells, device=dev, dtype=torch.int32), cnt)
+        pbs.append(ParticleBatch([a[perm].contiguous() for a in b.axes], cid[perm].contiguous(),
+                                 b.n_cells, b.n_bins, b.lo, b.hi))
+        del perm, cid
+    torch.cuda.empty_cache()
+    out = [None] * len(pbs)
+
+    def istep():
+        for i, pb in enumerate(pbs):
+            out[i] = compress_cells_indexed(pb, fcs[i], metas[i], keep_bins=False)
+
+    for _ in range(max(1, min(args.warmup, 2))):
+        istep()
+    torch.cuda.synchronize()
+    same = all(bool(torch.equal(out[i][2].weights, results[i].weights)) and
+               bool(torch.equal(out[i][2].iterations, results[i].iterations)) for i in range(len(pbs)))
+    barrier()
+    ctx.enable_timing(True)
+    ctx.reset_timing()
+    n_steps = max(1, min(args.steps, 3))
+    a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(n_steps):
+        istep()
+    b_.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b_) / n_steps
+    kt = ctx.kernel_times()
+    ctx.enable_timing(False)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    parts = sum(pb.n for pb in pbs)
+    tot = torch.tensor([float(parts)], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(tot)
+    group_ms = sum(v[0] for k, v in kt.items() if k.startswith("group_")) / n_steps
+    hist_ms = sum(v[0] for k, v in kt.items() if k.startswith("cells_") or k == "max_cell") / n_steps
+    algo = sum(pb.n * (d * 8 + 4) for pb in pbs)  # velocities + cell id read once
+    return {"value": float(tot.item()) / (ms * 1e-3), "unit": "particles/s", "ms_per_step": ms,
+            "order": "random permutation of the particles, int32 cell id per particle (device resident)",
+            "identical_results_to_grouped_path": same,
+            "group_ms": group_ms, "hist_ms": hist_ms,
+            "kernel_ms": {k: v[0] / n_steps for k, v in kt.items()},
+            "roofline_group_bin": {"bound": "hbm", "algorithmic_bytes": algo,
+                                   "achieved": algo / ((group_ms + hist_ms) * 1e-3) / 1e9 if group_ms + hist_ms else None,
+                                   "peak": hbm_peak, "unit": "GB/s",
+                                   "frac": algo / ((group_ms + hist_ms) * 1e-3) / 1e9 / hbm_peak if group_ms + hist_ms else None,
+                                   "algorithm": f"{d * 8 + 4} B/particle: u,v,w f64 + int32 cell id read once "
+                                                "(outputs excluded); time = grouping + per-cell binning kernels"}}
+
+
 def run_gpu(args, cfg):
     import torch
     import torch.distributed as dist
@@ -493,6 +560,14 @@ def run_gpu(args, cfg):
                          "algorithm": "24 B/particle read (u,v,w f64) + 12 B per non-empty bin "
                                       "written (u32 key + f64 count) + offsets"}
 
+    # ---- per-particle cell-index input (vdfcg_compress_cells_indexed): the same particles
+    # in a random order with an int32 cell id each, device resident; grouping + binning +
+    # fitting + packing inside the timed region
+    indexed = None
+    if not args.no_indexed and cfg["cells"] > 1:
+        indexed = run_indexed_leg(args, cfg, batches, fcs, metas, results, ctx, stream, dev,
+                                  hbm_peak, world, barrier)
+
     # ---- e2e through the public API: pinned host inputs, H2D + D2H inside the timed region
     e2e = None
     if not args.no_e2e:
@@ -587,7 +662,7 @@ def run_gpu(args, cfg):
             "gpu_launches": int(launches),
             "kernel_ms": {k: v[0] / args.steps for k, v in ktimes.items()},
             "roofline": roofline, "roofline_hist": roofline_hist,
-            "e2e": e2e, "cpu_baseline": cpu, "parity_sample": parity,
+            "e2e": e2e, "cpu_baseline": cpu, "parity_sample": parity, "indexed": indexed,
             "clocks": clk.summary(),
             "peaks": {"fp64_tflops": fp64_peak, "fp32_tflops": fp32_peak, "hbm_gbs": hbm_peak},
             "nnz_bins": nnz_tot,
@@ -609,6 +684,7 @@ def main():
     ap.add_argument("--ref-cells", type=int, default=256, help="reference arm cells/species/step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-indexed", action="store_true", help="skip the cell-index input leg")
     ap.add_argument("--estep-fp32", action="store_true",
                     help="FP32 E-step with FP64 accumulation (tolerance 1e-4, not the default)")
     args = ap.parse_args()

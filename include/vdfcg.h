@@ -366,6 +366,42 @@ int vdfcg_compress_cells_warm(vdfcg_ctx* ctx, const vdfcg_cells* cells,
                               const vdfcg_model_meta* meta, uint8_t* records, int64_t capacity,
                               int64_t* record_offsets);
 
+/* ---- Per-particle cell-index input (north_star: "streams particle (u,v,w) and cell-index
+ * arrays"). The particles of one species in ANY order, each with an int32 cell id — the
+ * device-side equivalent of the reference's per-part fan-out (split_subdomains then
+ * fit_one_plane per part, pipeline.cpp:76-104,130-160,340-345) for a caller that owns a PIC
+ * particle array. The library groups the particles by cell with a stable device sort (each
+ * cell keeps its particles in input order, so fractional weights are summed in the order of
+ * the reference's sequential `counts(i,j) += w`, histogram.cpp:66-74), then bins and fits
+ * exactly like the cell-grouped path. Cell c of the results is cell id c. */
+typedef struct vdfcg_particles {
+  int32_t dimension;            /* 2 or 3 velocity axes */
+  int64_t n_particles;          /* < 2^32 per call */
+  const double* velocity[3];    /* SoA axis arrays u, v, w; each n_particles, any order */
+  const double* weights;        /* NULL = unit weights */
+  const int32_t* cell;          /* [n_particles] cell id of each particle, in [0, n_cells) */
+  int32_t n_cells;
+  int32_t n_bins;               /* per axis; bins^d flat index (i*n+j)*n+k */
+  double lo[3];
+  double hi[3];
+} vdfcg_particles;
+
+/* Histogram every cell of an unsorted particle array. cell_offsets (out, [n_cells+1]) is
+ * the CSR of the grouped particles (cell c owned off[c+1]-off[c] of them); `out` is indexed
+ * by it exactly as vdfcg_bin_cells' output, so vdfcg_fit_cells / vdfcg_metrics_cells accept
+ * (a vdfcg_cells with these offsets, out). A cell id outside [0, n_cells) is an
+ * invalid_argument ("cell index out of range"). */
+int vdfcg_bin_cells_indexed(vdfcg_ctx* ctx, const vdfcg_particles* particles,
+                            int64_t* cell_offsets, vdfcg_cell_bins* out);
+
+/* bin_cells_indexed -> fit_cells (-> pack_cells when records != NULL) on one stream.
+ * cell_offsets and bins may be NULL (workspace). */
+int vdfcg_compress_cells_indexed(vdfcg_ctx* ctx, const vdfcg_particles* particles,
+                                 const vdfcg_fit_config* cfg, int64_t* cell_offsets,
+                                 vdfcg_cell_bins* bins, vdfcg_cell_results* out,
+                                 const vdfcg_model_meta* meta, uint8_t* records,
+                                 int64_t capacity, int64_t* record_offsets);
+
 /* Synthetic cell data for tests/bench (counter-based, deterministic per (seed, species,
  * global particle index)): each cell draws from a 2-component mixture whose drift and
  * temperature vary with the global cell index. cell_offsets are GLOBAL particle offsets

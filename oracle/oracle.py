@@ -72,6 +72,7 @@ _lib.oracle_mixture_moments.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
 _lib.oracle_weighted_data_moments.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
                                               C.c_void_p, C.c_void_p]
 _lib.oracle_bin_cells.argtypes = [C.c_void_p, C.c_void_p]
+_lib.oracle_bin_cells_indexed.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
 _lib.oracle_compress_cells.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                        C.c_void_p, C.c_void_p]
 _lib.oracle_evaluate_pdf.argtypes = [C.c_void_p, C.c_int32, C.c_double, C.c_double, C.c_double,
@@ -248,6 +249,41 @@ def bin_cells(cells: CellsHost) -> CellBinsHost:
     out = CellBinsHost(cells.n, cells.n_cells)
     _marshal.check(_lib.oracle_bin_cells(C.byref(cells.struct), C.byref(out.struct)), _err)
     return out
+
+
+class ParticlesHost:
+    """Host arrays of an unsorted particle set with a per-particle cell id (vdfcg_particles)."""
+
+    def __init__(self, velocity: np.ndarray, cell: np.ndarray, n_cells: int, n_bins: int, lo, hi,
+                 weights: np.ndarray | None = None):
+        self.velocity = np.asfortranarray(velocity, dtype=np.float64)  # N x d
+        self.cell = np.ascontiguousarray(cell, dtype=np.int32)
+        self.weights = None if weights is None else np.ascontiguousarray(weights, dtype=np.float64)
+        n, d = self.velocity.shape
+        self.n, self.d, self.n_cells = n, d, int(n_cells)
+        s = _abi.Particles()
+        s.dimension = d
+        s.n_particles = n
+        base = self.velocity.ctypes.data
+        for a in range(d):
+            s.velocity[a] = base + a * n * 8
+        s.weights = self.weights.ctypes.data if self.weights is not None else None
+        s.cell = self.cell.ctypes.data
+        s.n_cells = self.n_cells
+        s.n_bins = n_bins
+        for a in range(d):
+            s.lo[a] = float(lo[a])
+            s.hi[a] = float(hi[a])
+        self.struct = s
+
+
+def bin_cells_indexed(particles: ParticlesHost) -> tuple[np.ndarray, CellBinsHost]:
+    """Stable group-by-cell + per-cell binning; returns (cell_offsets, bins)."""
+    out = CellBinsHost(particles.n, particles.n_cells)
+    offsets = np.zeros(particles.n_cells + 1, dtype=np.int64)
+    _marshal.check(_lib.oracle_bin_cells_indexed(C.byref(particles.struct), offsets.ctypes.data,
+                                                 C.byref(out.struct)), _err)
+    return offsets, out
 
 
 def compress_cells(cells: CellsHost, config: FitConfig, cell_begin: int = 0,

@@ -1310,6 +1310,48 @@ int oracle_bin_cells(const vdfcg_cells* cells, vdfcg_cell_bins* out) {
   });
 }
 
+// Per-particle cell ids (vdfcg_particles): a stable counting sort by cell id keeps every
+// cell's particles in input order (the sequential order the reference would sum a part's
+// weights in, histogram.cpp:66-74), then each cell is binned as above. offsets: [n_cells+1].
+int oracle_bin_cells_indexed(const vdfcg_particles* p, int64_t* offsets, vdfcg_cell_bins* out) {
+  return guarded([&] {
+    const int64_t n = p->n_particles;
+    const int nc = p->n_cells;
+    std::vector<int64_t> cnt(size_t(nc) + 1, 0);
+    for (int64_t i = 0; i < n; ++i) {
+      const int32_t c = p->cell[i];
+      if (c < 0 || c >= nc) throw std::invalid_argument("cell index out of range");
+      ++cnt[size_t(c) + 1];
+    }
+    for (int c = 0; c < nc; ++c) cnt[size_t(c) + 1] += cnt[size_t(c)];
+    for (int c = 0; c <= nc; ++c) offsets[c] = cnt[size_t(c)];
+    const int d = p->dimension;
+    std::vector<double> vel(size_t(d) * size_t(n)), w(p->weights ? size_t(n) : 0);
+    std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t r = pos[size_t(p->cell[i])]++;
+      for (int a = 0; a < d; ++a) vel[size_t(a) * n + r] = p->velocity[a][i];
+      if (p->weights) w[size_t(r)] = p->weights[i];
+    }
+    vdfcg_cells cells{};
+    cells.dimension = d;
+    cells.n_particles = n;
+    for (int a = 0; a < d; ++a) cells.velocity[a] = vel.data() + size_t(a) * n;
+    cells.weights = p->weights ? w.data() : nullptr;
+    cells.n_cells = nc;
+    cells.cell_offsets = offsets;
+    cells.n_bins = p->n_bins;
+    for (int a = 0; a < 3; ++a) {
+      cells.lo[a] = p->lo[a];
+      cells.hi[a] = p->hi[a];
+    }
+    std::vector<double> dense;
+    for (int c = 0; c < nc; ++c)
+      bin_one_cell(&cells, c, dense, out->keys, out->counts, &out->nnz[c], &out->out_of_range[c],
+                   &out->in_range[c]);
+  });
+}
+
 int oracle_compress_cells(const vdfcg_cells* cells, const vdfcg_fit_config* cfg,
                           int32_t cell_begin, int32_t cell_end, int32_t threads,
                           vdfcg_cell_bins* bins, vdfcg_cell_results* out) {

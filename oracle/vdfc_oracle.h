@@ -84,6 +84,9 @@ int oracle_encode_model(const vdfcg_model* model, const vdfcg_model_meta* meta, 
 
 /* 3V/2V per-cell generalisation: bin + compact each cell. */
 int oracle_bin_cells(const vdfcg_cells* cells, vdfcg_cell_bins* out);
+/* Per-particle cell ids: stable group-by-cell, then oracle_bin_cells. offsets [n_cells+1]. */
+int oracle_bin_cells_indexed(const vdfcg_particles* particles, int64_t* offsets,
+                             vdfcg_cell_bins* out);
 /* The CPU baseline unit (pipeline.cpp:130-151): per cell bin + compact + fit, on a pool
  * of `threads` workers (0 = hardware concurrency), cells [cell_begin, cell_end). */
 int oracle_compress_cells(const vdfcg_cells* cells, const vdfcg_fit_config* cfg,

@@ -66,6 +66,13 @@ class Cells(C.Structure):
                 ("hi", C.c_double * 3)]
 
 
+class Particles(C.Structure):
+    _fields_ = [("dimension", C.c_int32), ("n_particles", C.c_int64),
+                ("velocity", C.c_void_p * 3), ("weights", C.c_void_p), ("cell", C.c_void_p),
+                ("n_cells", C.c_int32), ("n_bins", C.c_int32), ("lo", C.c_double * 3),
+                ("hi", C.c_double * 3)]
+
+
 class CellBins(C.Structure):
     _fields_ = [("nnz", C.c_void_p), ("keys", C.c_void_p), ("counts", C.c_void_p),
                 ("out_of_range", C.c_void_p), ("in_range", C.c_void_p)]

@@ -59,6 +59,8 @@ def _bind(lib) -> None:
         "vdfcg_compress_cells": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, i64, vp]),
         "vdfcg_fit_cells_warm": (C.c_int, [vp, vp, vp, vp, vp, vp]),
         "vdfcg_compress_cells_warm": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, i64, vp]),
+        "vdfcg_bin_cells_indexed": (C.c_int, [vp, vp, vp, vp]),
+        "vdfcg_compress_cells_indexed": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, i64, vp]),
         "vdfcg_synth_cells": (C.c_int, [vp, i32, i32, vp, i64, u64, i32, vp, vp, vp]),
         "vdfcg_probe_peaks": (C.c_int, [vp, vp, vp]),
         "vdfcg_generate": (C.c_int, [vp, i32, i32, vp, vp, vp, i64, u64, vp, vp]),

@@ -265,6 +265,101 @@ def compress_cells(batch: CellBatch, config: FitConfig, meta: Optional[ModelMeta
     return bins, results, rec, offs
 
 
+class ParticleBatch:
+    """Particles of one species in ANY order with an int32 cell id each (vdfcg_particles):
+    the per-particle cell-index input of a PIC code. velocity: d axis arrays (or an (n, d)
+    array), cell: n int32 ids in [0, n_cells)."""
+
+    def __init__(self, velocity, cell, n_cells: int, n_bins: int, lo, hi, weights=None):
+        if not isinstance(velocity, (list, tuple)):
+            if _is_torch(velocity):
+                velocity = [velocity[:, a].contiguous() for a in range(velocity.shape[1])]
+            else:
+                v = np.asarray(velocity, dtype=np.float64)
+                velocity = [np.ascontiguousarray(v[:, a]) for a in range(v.shape[1])]
+        self.axes = list(velocity)
+        self.d = len(self.axes)
+        self.cell = cell
+        self.weights = weights
+        self.n_cells = int(n_cells)
+        self.n_bins = int(n_bins)
+        self.lo = [float(x) for x in lo]
+        self.hi = [float(x) for x in hi]
+        self.n = int(self.axes[0].shape[0])
+        s = _abi.Particles()
+        s.dimension = self.d
+        s.n_particles = self.n
+        for a in range(self.d):
+            s.velocity[a] = _ptr(self.axes[a])
+        s.weights = _ptr(weights)
+        s.cell = _ptr(cell)
+        s.n_cells = self.n_cells
+        s.n_bins = self.n_bins
+        for a in range(self.d):
+            s.lo[a] = self.lo[a]
+            s.hi[a] = self.hi[a]
+        self.struct = s
+
+    def grouped(self, cell_offsets) -> CellBatch:
+        """The cell-grouped view for fit_cells / cell_metrics (which read only the geometry
+        and cell_offsets, never the velocities — these stay in the caller's order)."""
+        return CellBatch(self.axes, cell_offsets, self.n_bins, self.lo, self.hi, self.weights)
+
+
+def bin_cells_indexed(batch: ParticleBatch, out: Optional[CellBins] = None):
+    """Histogram every cell of an unsorted particle array. Returns (cell_offsets, bins);
+    bins are indexed by cell_offsets exactly like bin_cells' output."""
+    api = _api()
+    like = batch.axes[0]
+    offs = _empty(like, (batch.n_cells + 1,), "i64")
+    if out is None:
+        out = CellBins(_empty(like, (batch.n_cells,), "i32"), _empty(like, (max(batch.n, 1),), "u32"),
+                       _empty(like, (max(batch.n, 1),), "f64"), _empty(like, (batch.n_cells,), "f64"),
+                       _empty(like, (batch.n_cells,), "f64"))
+    bs = out.struct()
+    _check(api.lib().vdfcg_bin_cells_indexed(_ctx(like).handle, C.byref(batch.struct), _ptr(offs),
+                                             C.byref(bs)))
+    return offs, out
+
+
+def compress_cells_indexed(batch: ParticleBatch, config: FitConfig,
+                           meta: Optional[ModelMeta] = None, trace: bool = False,
+                           keep_bins: bool = True):
+    """group by cell -> bin -> fit (-> pack) on the device. Returns
+    (cell_offsets, bins, results, records, record_offsets); cell c is cell id c."""
+    api = _api()
+    d = batch.d
+    wm = _abi.ModelBuffers.from_model(config.warm_start) if config.warm_start is not None else None
+    cfg = _abi.fit_config_struct(config, d, wm)
+    k = max(config.initial_components, wm.k if wm else 0)
+    like = batch.axes[0]
+    offs = _empty(like, (batch.n_cells + 1,), "i64")
+    bins = None
+    if keep_bins:
+        bins = CellBins(_empty(like, (batch.n_cells,), "i32"), _empty(like, (max(batch.n, 1),), "u32"),
+                        _empty(like, (max(batch.n, 1),), "f64"), _empty(like, (batch.n_cells,), "f64"),
+                        _empty(like, (batch.n_cells,), "f64"))
+    results = CellResults(like, batch.n_cells, d, k, config.max_em_iterations if trace else 0)
+    bs = bins.struct() if bins is not None else None
+    rs = results.struct()
+    rec = roffs = None
+    cap = 0
+    ms = None
+    if meta is not None:
+        ms, _keep = _abi.meta_struct(meta, d)
+        per = 26 + 16 * d + ms.label_len + k * (1 + d + d * (d + 1) // 2) * 8
+        cap = batch.n_cells * per
+        rec = _empty(like, (max(cap, 1),), "u8")
+        roffs = _empty(like, (batch.n_cells + 1,), "i64")
+    _check(api.lib().vdfcg_compress_cells_indexed(
+        _ctx(like, results.weights).handle, C.byref(batch.struct), C.byref(cfg), _ptr(offs),
+        C.byref(bs) if bs is not None else None, C.byref(rs),
+        C.byref(ms) if ms is not None else None, _ptr(rec), cap, _ptr(roffs)))
+    if rec is not None:
+        rec = rec[:int(roffs[-1])]
+    return offs, bins, results, rec, roffs
+
+
 class CellMetrics:
     """Per-cell MetricsReport fields (vdfcg_cell_metrics), one array per field."""
 

@@ -1119,6 +1119,115 @@ int vdfcg_compress_cells_warm(vdfcg_ctx* ctx, const vdfcg_cells* cells,
   });
 }
 
+// ---- per-particle cell-index input (index.cu) ---------------------------------------
+// Validation as stage_cells, plus the cell ids; returns the staged device view.
+static IndexedDev stage_particles(vdfcg_ctx* ctx, const vdfcg_particles* p) {
+  if (!p) throw InvalidArgument("null particles");
+  const int d = p->dimension;
+  if (d != 2 && d != 3) throw InvalidArgument("particle dimension must be 2 or 3");
+  if (p->n_bins < 2) throw InvalidArgument("n_bins must be >= 2");
+  double nbd = 1.0;
+  for (int a = 0; a < d; ++a) nbd *= p->n_bins;
+  if (nbd > 2147483647.0) throw InvalidArgument("n_bins^d must fit a 31-bit bin key");
+  for (int a = 0; a < d; ++a)
+    if (!range_ok(p->lo[a], p->hi[a])) throw InvalidArgument("axis range must satisfy min < max");
+  if (p->n_cells < 1 || p->n_particles < 0) throw InvalidArgument("negative sizes");
+  if (p->n_particles >= (int64_t(1) << 32)) throw InvalidArgument("cell-index input supports < 2^32 particles per call");
+  if (p->n_particles && !p->cell) throw InvalidArgument("cell index array is required");
+  IndexedDev in{};
+  in.d = d;
+  in.n = p->n_particles;
+  for (int a = 0; a < d; ++a) {
+    if (!p->velocity[a] && in.n) throw InvalidArgument("missing velocity axis");
+    in.vel[a] = stage_in(ctx, p->velocity[a], size_t(in.n)).dev;
+  }
+  for (int a = d; a < 3; ++a) in.vel[a] = in.vel[0];
+  in.w = p->weights ? stage_in(ctx, p->weights, size_t(in.n)).dev : nullptr;
+  in.cell = stage_in(ctx, p->cell, size_t(in.n)).dev;
+  in.n_cells = p->n_cells;
+  in.n_bins = p->n_bins;
+  for (int a = 0; a < 3; ++a) {
+    in.lo[a] = p->lo[a];
+    in.hi[a] = p->hi[a];
+  }
+  return in;
+}
+
+// Group by cell, then the CellsDev view of the grouped keys (velocities are not needed
+// past the grouping: the bin key was computed while they were read).
+static CellsDev group_particles(vdfcg_ctx* ctx, const IndexedDev& in, int64_t* offsets_dev, int* err) {
+  GroupedDev g{arena<uint32_t>(ctx, size_t(std::max<int64_t>(in.n, 1))),
+               in.w ? arena<double>(ctx, size_t(std::max<int64_t>(in.n, 1))) : nullptr, offsets_dev};
+  launch_group_cells(ctx, in, g, err);
+  CellsDev c{};
+  c.d = in.d;
+  c.n = in.n;
+  for (int a = 0; a < 3; ++a) c.vel[a] = nullptr;
+  c.w = g.w;
+  c.n_cells = in.n_cells;
+  c.offsets = offsets_dev;
+  c.n_bins = in.n_bins;
+  for (int a = 0; a < 3; ++a) {
+    c.lo[a] = in.lo[a];
+    c.hi[a] = in.hi[a];
+  }
+  c.keys = g.keys;
+  return c;
+}
+
+static void check_group_error(vdfcg_ctx* ctx, const int* err) {
+  const int e = read_scalar(ctx, err);
+  if (e & 1) throw InvalidArgument("cell index out of range");
+  if (e & 2) throw InvalidArgument("particle weights must all be > 0");
+}
+
+int vdfcg_bin_cells_indexed(vdfcg_ctx* ctx, const vdfcg_particles* particles, int64_t* cell_offsets,
+                            vdfcg_cell_bins* out) {
+  return guard_impl([&] {
+    begin(ctx);
+    IndexedDev in = stage_particles(ctx, particles);
+    if (!out || !cell_offsets) throw InvalidArgument("null output");
+    int* err = arena<int>(ctx, 1);
+    VDFCG_CUDA(cudaMemsetAsync(err, 0, sizeof(int), ctx->stream));
+    auto offs = stage_out(ctx, cell_offsets, size_t(in.n_cells) + 1);
+    CellsDev c = group_particles(ctx, in, offs.dev, err);
+    check_group_error(ctx, err);
+    std::vector<std::function<void()>> fin;
+    CellBinsDev b = bins_dev(ctx, c, out, fin);
+    launch_bin_cells(ctx, c, b);
+    finish(ctx, offs);
+    for (auto& f : fin) f();
+    sync(ctx);
+  });
+}
+
+int vdfcg_compress_cells_indexed(vdfcg_ctx* ctx, const vdfcg_particles* particles,
+                                 const vdfcg_fit_config* cfg, int64_t* cell_offsets,
+                                 vdfcg_cell_bins* bins, vdfcg_cell_results* out,
+                                 const vdfcg_model_meta* meta, uint8_t* records, int64_t capacity,
+                                 int64_t* record_offsets) {
+  return guard_impl([&] {
+    begin(ctx);
+    IndexedDev in = stage_particles(ctx, particles);
+    validate_config(cfg, in.d);
+    int* err = arena<int>(ctx, 1);
+    VDFCG_CUDA(cudaMemsetAsync(err, 0, sizeof(int), ctx->stream));
+    auto offs = stage_out(ctx, cell_offsets, cell_offsets ? size_t(in.n_cells) + 1 : 0);
+    int64_t* offs_dev = offs.dev ? offs.dev : arena<int64_t>(ctx, size_t(in.n_cells) + 1);
+    CellsDev c = group_particles(ctx, in, offs_dev, err);
+    check_group_error(ctx, err);
+    std::vector<std::function<void()>> fin;
+    CellBinsDev b = bins_dev(ctx, c, bins, fin);
+    EmOut o = results_dev(ctx, c.n_cells, c.d, out, fin);
+    launch_bin_cells(ctx, c, b);
+    fit_cells_dev(ctx, c, b, cfg, o);
+    pack_into(ctx, c, o, meta, records, capacity, record_offsets, fin);
+    finish(ctx, offs);
+    for (auto& f : fin) f();
+    sync(ctx);
+  });
+}
+
 // ---- fit quality --------------------------------------------
 // GmmModel::validate (wgmm.cpp:46-63) on the device, then the staged model.
 static ModelDev staged_valid_model(vdfcg_ctx* ctx, const vdfcg_model* model) {

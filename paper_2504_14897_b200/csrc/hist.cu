@@ -295,22 +295,30 @@ struct CellGeom {
   double lo[3], hi[3], inv[3];
 };
 
-template <int D>
-VDFCG_DEV int64_t cell_key(const double* const* vel, int64_t i, const CellGeom& g) {
-  int64_t key = 0;
-  bool out = false;
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    const int b = bin_index(__ldg(vel[a] + i), g.lo[a], g.hi[a], g.n_bins, g.inv[a]);
-    out |= b < 0;
-    key = key * g.n_bins + b;
-  }
-  return out ? -1 : key;
-}
-
 struct VelPtrs {
   const double* v[3];
+  const uint32_t* keys;  // D == 0: precomputed bin keys (0xffffffff = out of range)
 };
+
+// Flat bin key of particle i, -1 when out of range. D == 0 reads a key
+// computed upstream (the cell-index path, index.cu) instead of the velocities.
+template <int D>
+VDFCG_DEV int64_t cell_key(const VelPtrs& vp, int64_t i, const CellGeom& g) {
+  if constexpr (D == 0) {
+    const uint32_t k = __ldg(vp.keys + i);
+    return k == 0xffffffffu ? int64_t(-1) : int64_t(k);
+  } else {
+    int64_t key = 0;
+    bool out = false;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const int b = bin_index(__ldg(vp.v[a] + i), g.lo[a], g.hi[a], g.n_bins, g.inv[a]);
+      out |= b < 0;
+      key = key * g.n_bins + b;
+    }
+    return out ? -1 : key;
+  }
+}
 
 // K2: work item = (cell, chunk of `chunk` particles).
 template <int D, bool SMEM>
@@ -347,7 +355,7 @@ __global__ void __launch_bounds__(1024) cells_dense_kernel(
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t i = i0 + int64_t(u) * blockDim.x;
-        key[u] = i < e ? cell_key<D>(vp.v, i, g) : -2;
+        key[u] = i < e ? cell_key<D>(vp, i, g) : -2;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -470,7 +478,7 @@ __global__ void __launch_bounds__(BLOCK) cells_sort_kernel(
     for (int i = 0; i < IPT; ++i) {
       const int li = i * BLOCK + threadIdx.x;  // striped, coalesced loads
       if (li < nc) {
-        const int64_t key = cell_key<D>(vp.v, b + li, g);
+        const int64_t key = cell_key<D>(vp, b + li, g);
         const uint32_t bin = key < 0 ? sent : static_cast<uint32_t>(key);
         k[i] = W ? ((bin << idxbits) | static_cast<uint32_t>(li)) : bin;
         if (W) bad |= !(__ldg(w + b + li) > 0.0);
@@ -588,7 +596,7 @@ __global__ void __launch_bounds__(BLOCK) cells_bitmap_kernel(
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int li = l0 + u * BLOCK;
-        key[u] = li < nc ? cell_key<D>(vp.v, b + li, g) : -2;
+        key[u] = li < nc ? cell_key<D>(vp, b + li, g) : -2;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -625,7 +633,7 @@ __global__ void __launch_bounds__(BLOCK) cells_bitmap_kernel(
       if (li < cap) {
         key = kbuf[li];
       } else {
-        const int64_t k2 = cell_key<D>(vp.v, b + li, g);
+        const int64_t k2 = cell_key<D>(vp, b + li, g);
         key = k2 < 0 ? 0xffffffffu : static_cast<unsigned>(k2);
       }
       if (key != 0xffffffffu) {
@@ -659,6 +667,7 @@ __global__ void __launch_bounds__(BLOCK) cells_bitmap_kernel(
 // slices into the same buffer, so the HBM reads of cell c+grid overlap the rank / count
 // / emit phases of cell c and no warp waits on global-load latency. Slices are widened
 // to 16-byte boundaries (bulk-copy granularity); `skew` locates the cell inside them.
+// D == 0 stages the cell's precomputed u32 bin keys instead (cell-index path).
 VDFCG_DEV uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -687,39 +696,77 @@ VDFCG_DEV void bar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-// Stage cell c's axis slices. The 16-byte widening never reads past element lim-1
-// (lim = offsets[n_cells]): an odd last element is loaded by this thread directly.
+// Stage cell c's axis slices (D == 0: its precomputed u32 keys). Axis a's base address is
+// `sh[a]` elements past a 16-byte boundary (an Eigen N x 3 column of odd N starts 8 bytes
+// off), so element x is 16-byte aligned iff (x + sh[a]) % A == 0, A = 16 / element size.
+// The staged window is [B, E) with B = floor_A(b + sh) - sh, E = ceil_A(e + sh) - sh, kept
+// at pbuf[a][x - B] (skew b - B); the part a bulk copy may not touch — before element 0 or
+// past element lim-1 (lim = offsets[n_cells]) — is loaded by this thread directly.
+template <int D>
+struct Stage {
+  static constexpr int kArrays = D == 0 ? 1 : D;
+  static constexpr int kElem = D == 0 ? 4 : 8;
+  static constexpr int kA = 16 / kElem;
+};
+
 template <int D>
 VDFCG_DEV void issue_cell_copy(const VelPtrs& vp, const int64_t* offsets, int c, int64_t lim,
-                               double* pbuf, int capp, uint64_t* bar) {
+                               unsigned char* pbuf, int capp, const int* sh, uint64_t* bar) {
+  using S = Stage<D>;
+  constexpr int A = S::kA;
   const int64_t b = offsets[c], e = offsets[c + 1];
-  const int64_t b0 = b & ~int64_t(1);
-  int64_t e0 = (e + 1) & ~int64_t(1);
-  const bool tail = e0 > lim;  // e == lim, odd
-  if (tail) e0 -= 2;
-  const uint32_t bytes = e0 > b0 ? static_cast<uint32_t>((e0 - b0) * 8) : 0u;
-  if (tail)
+  uint32_t total = 0;
+  int64_t bb[S::kArrays], ee[S::kArrays], B[S::kArrays];
 #pragma unroll
-    for (int a = 0; a < D; ++a) pbuf[a * capp + (e0 - b0)] = __ldg(vp.v[a] + e0);
+  for (int a = 0; a < S::kArrays; ++a) {
+    B[a] = ((b + sh[a]) / A) * A - sh[a];
+    const int64_t E = ((e + sh[a] + A - 1) / A) * A - sh[a];
+    bb[a] = B[a] < 0 ? B[a] + A : B[a];
+    ee[a] = E > lim ? E - A : E;
+    if (ee[a] < bb[a]) ee[a] = bb[a];
+    // direct loads of [b, e) outside the bulk window [bb, ee)
+    for (int64_t x = b; x < e; ++x) {
+      if (x >= bb[a] && x < ee[a]) {
+        x = ee[a] - 1;
+        continue;
+      }
+      if constexpr (D == 0)
+        reinterpret_cast<uint32_t*>(pbuf)[x - B[a]] = __ldg(vp.keys + x);
+      else
+        reinterpret_cast<double*>(pbuf)[a * capp + (x - B[a])] = __ldg(vp.v[a] + x);
+    }
+    total += static_cast<uint32_t>((ee[a] - bb[a]) * S::kElem);
+  }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  bar_expect(bar, bytes * D);
-  if (bytes)
+  bar_expect(bar, total);
 #pragma unroll
-    for (int a = 0; a < D; ++a) bulk_g2s(pbuf + a * capp, vp.v[a] + b0, bytes, bar);
+  for (int a = 0; a < S::kArrays; ++a) {
+    const uint32_t bytes = static_cast<uint32_t>((ee[a] - bb[a]) * S::kElem);
+    if (!bytes) continue;
+    if constexpr (D == 0)
+      bulk_g2s(reinterpret_cast<uint32_t*>(pbuf) + (bb[a] - B[a]), vp.keys + bb[a], bytes, bar);
+    else
+      bulk_g2s(reinterpret_cast<double*>(pbuf) + a * capp + (bb[a] - B[a]), vp.v[a] + bb[a], bytes, bar);
+  }
 }
+
+struct StageShift {
+  int sh[3];
+};
 
 template <int D, int BLOCK, int kTmaWpt>  // kTmaWpt >= bitmap words per thread
 __global__ void __launch_bounds__(BLOCK) cells_bitmap_tma_kernel(
     VelPtrs vp, const int64_t* __restrict__ offsets, int n_cells, CellGeom g, int words, int ccap,
-    int capp, int32_t* nnz, uint32_t* __restrict__ keys_out, double* __restrict__ counts_out,
-    double* oor_out, double* in_range) {
+    int capp, StageShift ss_, int32_t* nnz, uint32_t* __restrict__ keys_out,
+    double* __restrict__ counts_out, double* oor_out, double* in_range) {
   using Scan = cub::BlockScan<unsigned, BLOCK>;
   __shared__ typename Scan::TempStorage ss;
   __shared__ unsigned s_oor;
   __shared__ __align__(8) uint64_t bar;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* pbuf = reinterpret_cast<double*>(smem_raw);                    // [D][capp]
-  unsigned* bitmap = reinterpret_cast<unsigned*>(pbuf + D * capp);       // [words]
+  using S = Stage<D>;
+  unsigned char* pbuf = smem_raw;                                        // [arrays][capp]
+  unsigned* bitmap = reinterpret_cast<unsigned*>(pbuf + size_t(S::kArrays) * capp * S::kElem);
   unsigned* wpre = bitmap + words;                                       // [words]
   unsigned* cnt = wpre + words;                                          // [ccap]
   unsigned* kbuf = cnt + ccap;                                           // [capp]
@@ -732,14 +779,16 @@ __global__ void __launch_bounds__(BLOCK) cells_bitmap_tma_kernel(
     s_oor = 0u;
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (blockIdx.x < n_cells) issue_cell_copy<D>(vp, offsets, blockIdx.x, lim, pbuf, capp, &bar);
+    if (blockIdx.x < n_cells) issue_cell_copy<D>(vp, offsets, blockIdx.x, lim, pbuf, capp, ss_.sh, &bar);
   }
   __syncthreads();
   uint32_t parity = 0;
   for (int c = blockIdx.x; c < n_cells; c += gridDim.x) {
     const int64_t b = offsets[c];
     const int nc = static_cast<int>(offsets[c + 1] - b);
-    const int skew = static_cast<int>(b & 1);
+    int skew[S::kArrays];
+#pragma unroll
+    for (int a = 0; a < S::kArrays; ++a) skew[a] = static_cast<int>((b + ss_.sh[a]) % S::kA);
     bar_wait(&bar, parity);
     parity ^= 1u;
     // 1. occupancy bits from the staged slices
@@ -747,11 +796,18 @@ __global__ void __launch_bounds__(BLOCK) cells_bitmap_tma_kernel(
     for (int li = threadIdx.x; li < nc; li += BLOCK) {
       int64_t key = 0;
       bool out = false;
+      if constexpr (D == 0) {
+        const uint32_t k = reinterpret_cast<const uint32_t*>(pbuf)[skew[0] + li];
+        out = k == 0xffffffffu;
+        key = k;
+      } else {
+        const double* pb = reinterpret_cast<const double*>(pbuf);
 #pragma unroll
-      for (int a = 0; a < D; ++a) {
-        const int bi = bin_index(pbuf[a * capp + skew + li], g.lo[a], g.hi[a], g.n_bins, g.inv[a]);
-        out |= bi < 0;
-        key = key * g.n_bins + bi;
+        for (int a = 0; a < D; ++a) {
+          const int bi = bin_index(pb[a * capp + skew[a] + li], g.lo[a], g.hi[a], g.n_bins, g.inv[a]);
+          out |= bi < 0;
+          key = key * g.n_bins + bi;
+        }
       }
       if (out) {
         ++oor;
@@ -766,7 +822,7 @@ __global__ void __launch_bounds__(BLOCK) cells_bitmap_tma_kernel(
     __syncthreads();
     // the staging buffer is free: fetch the next cell while this one is ranked
     if (threadIdx.x == 0 && c + static_cast<int>(gridDim.x) < n_cells)
-      issue_cell_copy<D>(vp, offsets, c + gridDim.x, lim, pbuf, capp, &bar);
+      issue_cell_copy<D>(vp, offsets, c + gridDim.x, lim, pbuf, capp, ss_.sh, &bar);
     // 2. ranks; the word popcounts stay in registers for the prefix and the re-zeroing
     unsigned local = 0, pc[kTmaWpt];
 #pragma unroll
@@ -881,7 +937,7 @@ static void launch_sort(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
   VDFCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, BLOCK, smem));
   const int grid = std::max(1, std::min(c.n_cells, ctx->sm_count * std::max(occ, 1)));
   const int idxbits = W ? bits_for(CAP - 1) : 0;
-  VelPtrs vp{{c.vel[0], c.vel[1], c.vel[2]}};
+  VelPtrs vp{{c.vel[0], c.vel[1], c.vel[2]}, c.keys};
   VDFCG_LAUNCH(ctx, "cells_sort",
                k<<<grid, BLOCK, smem, ctx->stream>>>(vp, c.w, c.offsets, c.n_cells, g, binbits,
                                                      idxbits, out.nnz, out.keys, out.counts,
@@ -900,12 +956,14 @@ static bool try_sort_path(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& 
   return true;
 }
 
+// D = velocity axes read by the kernels, or 0 when the bin keys were computed upstream
+// (c.keys, the cell-index path); the grid dimension is c.d either way.
 template <int D>
 static void bin_cells_d(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& out) {
   CellGeom g{};
   g.n_bins = c.n_bins;
   int64_t bins = 1;
-  for (int a = 0; a < D; ++a) {
+  for (int a = 0; a < c.d; ++a) {
     g.lo[a] = c.lo[a];
     g.hi[a] = c.hi[a];
     g.inv[a] = c.n_bins / (c.hi[a] - c.lo[a]);
@@ -924,12 +982,20 @@ static void bin_cells_d(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
   const int64_t words = (bins + 31) / 32;
   const int64_t ccap = std::max<int64_t>(1, std::min<int64_t>(maxc, bins));  // >= every nnz
   const int64_t kcap = std::min<int64_t>(maxc, 4096);
-  // TMA-staged variant: every axis base 16-byte aligned and the staging buffer (largest
-  // cell + 16-byte slack per axis) fits beside the bitmap with two CTAs per SM.
-  const int64_t capp = ((maxc + 2 + 1) / 2) * 2;
-  const size_t tma_smem = size_t(D) * capp * 8 + size_t(words) * 8 + size_t(ccap) * 8 + size_t(capp) * 4;
+  // TMA-staged variant: the staging window (largest cell + up to 16 bytes of widening at
+  // each end per array) fits beside the bitmap. Bases need only element alignment: the
+  // kernel carries each array's offset from a 16-byte boundary (Eigen N x 3 columns).
+  using S = Stage<D>;
+  const int64_t capp = ((maxc + 2 * (S::kA - 1) + S::kA - 1) / S::kA) * S::kA;
+  const size_t tma_smem = size_t(S::kArrays) * capp * S::kElem + size_t(words) * 8 + size_t(ccap) * 8 +
+                          size_t(capp) * 4;
   bool aligned = true;
-  for (int a = 0; a < D; ++a) aligned = aligned && (reinterpret_cast<uintptr_t>(c.vel[a]) & 15) == 0;
+  StageShift shift{};
+  for (int a = 0; a < S::kArrays; ++a) {
+    const uintptr_t addr = D == 0 ? reinterpret_cast<uintptr_t>(c.keys) : reinterpret_cast<uintptr_t>(c.vel[a]);
+    aligned = aligned && (addr % S::kElem) == 0;
+    shift.sh[a] = static_cast<int>((addr % 16) / S::kElem);
+  }
   static const int tma_env = [] {
     const char* e = getenv("VDFCG_HIST_TMA");  // 0: off, 1: 512-thread CTAs, 2: 256
     return e ? atoi(e) : 1;
@@ -965,10 +1031,10 @@ static void bin_cells_d(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
     int occ = 0;
     VDFCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, tb, tma_smem));
     const int grid = std::max(1, std::min(c.n_cells, ctx->sm_count * std::max(occ, 1)));
-    VelPtrs vp{{c.vel[0], c.vel[1], c.vel[2]}};
+    VelPtrs vp{{c.vel[0], c.vel[1], c.vel[2]}, c.keys};
     VDFCG_LAUNCH(ctx, "cells_bitmap_tma",
                  k<<<grid, tb, tma_smem, ctx->stream>>>(vp, c.offsets, c.n_cells, g, static_cast<int>(words),
-                                                        static_cast<int>(ccap), static_cast<int>(capp),
+                                                        static_cast<int>(ccap), static_cast<int>(capp), shift,
                                                         out.nnz, out.keys, out.counts, out.oor, out.in_range));
     done = true;
   }
@@ -980,7 +1046,7 @@ static void bin_cells_d(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
     int occ = 0;
     VDFCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, smem));
     const int grid = std::max(1, std::min(c.n_cells, ctx->sm_count * std::max(occ, 1)));
-    VelPtrs vp{{c.vel[0], c.vel[1], c.vel[2]}};
+    VelPtrs vp{{c.vel[0], c.vel[1], c.vel[2]}, c.keys};
     VDFCG_LAUNCH(ctx, "cells_bitmap",
                  k<<<grid, 256, smem, ctx->stream>>>(vp, c.offsets, c.n_cells, g, static_cast<int>(words),
                                                      static_cast<int>(ccap), cap, out.nnz, out.keys, out.counts, out.oor,
@@ -1022,7 +1088,7 @@ static void bin_cells_d(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
                                           ctx->stream>>>(c.offsets, c.n_cells, chunk, cpc));
     launch_scan_i64(ctx, cpc, item_off, c.n_cells);
     const int64_t est_items = (c.n + chunk - 1) / chunk + c.n_cells;
-    VelPtrs vp{{c.vel[0], c.vel[1], c.vel[2]}};
+    VelPtrs vp{{c.vel[0], c.vel[1], c.vel[2]}, c.keys};
     if (smem_ok) {
       const size_t smem = static_cast<size_t>(bins) * 4;
       auto k = cells_dense_kernel<D, true>;
@@ -1064,7 +1130,8 @@ static void bin_cells_d(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
 
 void launch_bin_cells(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& out) {
   if (c.n_cells == 0) return;
-  if (c.d == 2) bin_cells_d<2>(ctx, c, out);
+  if (c.keys) bin_cells_d<0>(ctx, c, out);
+  else if (c.d == 2) bin_cells_d<2>(ctx, c, out);
   else bin_cells_d<3>(ctx, c, out);
 }
 

@@ -32,6 +32,7 @@ struct CellsDev {
   int64_t max_cell = -1;   // largest cell, when the host already knows it (else computed)
   int shape_cells = 0;     // EM launch shape from the whole batch when > 0 (chunked calls)
   double shape_avg = 0.0;
+  const uint32_t* keys = nullptr;  // precomputed bin keys (cell-index path): vel unused
 };
 struct CellBinsDev {
   int32_t* nnz;
@@ -41,6 +42,27 @@ struct CellBinsDev {
   double* in_range;
 };
 void launch_bin_cells(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& out);
+
+// Cell-index input (index.cu): particles in any order with an int32 cell id each.
+struct IndexedDev {
+  int d;
+  int64_t n;  // < 2^32
+  const double* vel[3];
+  const double* w;
+  const int32_t* cell;
+  int n_cells;
+  int n_bins;
+  double lo[3], hi[3];
+};
+// Stable group-by-cell: keys (u32 bin key per particle, 0xffffffff = out of range) and
+// weights in cell order, offsets[n_cells+1]. err |= 1 on a cell id outside [0, n_cells),
+// |= 2 on a weight that is not > 0.
+struct GroupedDev {
+  uint32_t* keys;
+  double* w;
+  int64_t* offsets;
+};
+void launch_group_cells(vdfcg_ctx* ctx, const IndexedDev& in, const GroupedDev& out, int* err);
 
 // Exclusive scan of n int64 values (device), total written to out[n].
 void launch_scan_i64(vdfcg_ctx* ctx, const int64_t* in, int64_t* out, int64_t n);
