@@ -141,18 +141,16 @@ VDFCG_DEV void em_pass(const Src& src, int n, EmState<D, K>& S, double* red) {
     src.load(valid ? p : b0, z, w);
     if (!valid) w = 0.0;
     double lp[K];
-    double mx = -dinf();
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-      lp[j] = comp_logp2_affine<D>(z, S.A[j], S.bv[j], S.cst[j]);
-      mx = lp[j] > mx ? lp[j] : mx;
-    }
-    double sum = 0.0;
+    for (int j = 0; j < K; ++j) lp[j] = comp_logp2_affine<D>(z, S.A[j], S.bv[j], S.cst[j]);
+    double mx = lp[0];  // slot 0 is always active (m >= 1)
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-      lp[j] = exp2_nonpos(lp[j] - mx, S.exp2tab);
-      sum += lp[j];
-    }
+    for (int j = 1; j < K; ++j) mx = lp[j] > mx ? lp[j] : mx;
+#pragma unroll
+    for (int j = 0; j < K; ++j) lp[j] = exp2_nonpos(lp[j] - mx, S.exp2tab);
+    double sum = lp[0];
+#pragma unroll
+    for (int j = 1; j < K; ++j) sum += lp[j];
     if (!EXACT) ll += w * fma(mx, 0.6931471805599453, log_ge1(sum, S.logtab));
     const double ws = w * rcp_newton(sum);
     if (!EXACT) {
@@ -806,7 +804,10 @@ template <int D, int K, bool KEYS, bool F32 = false, bool CLU = false>
 #ifndef VDFCG_EM_MAXREG_K3
 #define VDFCG_EM_MAXREG_K3 128
 #endif
-__global__ void __launch_bounds__(256) __maxnreg__(K == 1 ? VDFCG_EM_MAXREG_K1 : K == 2 ? VDFCG_EM_MAXREG_K2 : K == 3 ? VDFCG_EM_MAXREG_K3 : (K <= 4 ? 128 : 255)) em_kernel(KeyCells kc, CoordArgs ca, EmConfig cfg,
+#ifndef VDFCG_EM_MAXREG_K4
+#define VDFCG_EM_MAXREG_K4 128
+#endif
+__global__ void __launch_bounds__(256) __maxnreg__(K == 1 ? VDFCG_EM_MAXREG_K1 : K == 2 ? VDFCG_EM_MAXREG_K2 : K == 3 ? VDFCG_EM_MAXREG_K3 : (K <= 4 ? VDFCG_EM_MAXREG_K4 : 255)) em_kernel(KeyCells kc, CoordArgs ca, EmConfig cfg,
                                                  EmOut out, int* counter, int red_stride) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   EmState<D, K>& S = *reinterpret_cast<EmState<D, K>*>(smem_raw);
