@@ -55,7 +55,10 @@ def dist_env():
 
 
 def cell_counts(cfg) -> np.ndarray:
-    """Particles per cell of one species: the total split as evenly as possible."""
+    """Particles per cell of one species: the total split as evenly as possible (or the
+    config's explicit "counts")."""
+    if "counts" in cfg:
+        return np.asarray(cfg["counts"], dtype=np.int64)
     c, n = cfg["cells"], cfg["particles"]
     base, extra = divmod(n, c)
     counts = np.full(c, base, dtype=np.int64)
@@ -64,10 +67,15 @@ def cell_counts(cfg) -> np.ndarray:
 
 
 def my_cells(cfg, rank, world):
+    """This rank's contiguous cell range, balanced by particle count (prefix
+    sum of the per-cell counts, vdfcg_partition_cells — host-only, no device needed)."""
     c = cfg["cells"]
-    if cfg["scaling"] == "replicas":
+    if cfg["scaling"] == "replicas" or world == 1:
         return 0, c
-    return rank * c // world, (rank + 1) * c // world
+    from paper_2504_14897_b200.cells import partition_cells
+    offs = np.concatenate([[0], np.cumsum(cell_counts(cfg))]).astype(np.int64)
+    b = partition_cells(offs, world)
+    return int(b[rank]), int(b[rank + 1])
 
 
 class ClockSampler:

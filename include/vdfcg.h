@@ -402,6 +402,32 @@ int vdfcg_compress_cells_indexed(vdfcg_ctx* ctx, const vdfcg_particles* particle
                                  const vdfcg_model_meta* meta, uint8_t* records,
                                  int64_t capacity, int64_t* record_offsets);
 
+/* ---- Several devices from one host process (run_pipeline's fan-out over
+ * parts and final gather, pipeline.cpp:340-353). Cells are independent, so a batch is split
+ * into contiguous cell ranges balanced by particle count and each device bins, fits and
+ * packs its range on its own context and host thread; no collective on the data path. The
+ * records of all devices are gathered in cell order into one host buffer with global
+ * offsets — byte-identical to a one-device call. */
+typedef struct vdfcg_multi vdfcg_multi;
+
+/* Contiguous cell ranges [cell_begin[r], cell_begin[r+1]) for n_parts workers with about
+ * (off[n_cells] - off[0]) / n_parts particles each (the cell boundary whose particle prefix
+ * is nearest r * total / n_parts). Host-only: needs no device. cell_begin: [n_parts + 1]. */
+int vdfcg_partition_cells(const int64_t* cell_offsets, int32_t n_cells, int32_t n_parts,
+                          int32_t* cell_begin);
+int vdfcg_multi_create(const int32_t* devices, int32_t n_devices, vdfcg_multi** out);
+int vdfcg_multi_destroy(vdfcg_multi* m);
+int32_t vdfcg_multi_device_count(const vdfcg_multi* m);
+/* The context of device slot `index` (e.g. to enable per-kernel timing). */
+int vdfcg_multi_context(vdfcg_multi* m, int32_t index, vdfcg_ctx** out);
+/* vdfcg_compress_cells over every device of `m`. Host buffers (cells->cell_offsets must be
+ * host memory); bins may be NULL; records/record_offsets as vdfcg_compress_cells over the
+ * whole batch. cell_begin (may be NULL) receives the partition used, [n_devices + 1]. */
+int vdfcg_multi_compress_cells(vdfcg_multi* m, const vdfcg_cells* cells, const vdfcg_fit_config* cfg,
+                               vdfcg_cell_bins* bins, vdfcg_cell_results* out,
+                               const vdfcg_model_meta* meta, uint8_t* records, int64_t capacity,
+                               int64_t* record_offsets, int32_t* cell_begin);
+
 /* Synthetic cell data for tests/bench (counter-based, deterministic per (seed, species,
  * global particle index)): each cell draws from a 2-component mixture whose drift and
  * temperature vary with the global cell index. cell_offsets are GLOBAL particle offsets

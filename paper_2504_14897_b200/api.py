@@ -61,6 +61,12 @@ def _bind(lib) -> None:
         "vdfcg_compress_cells_warm": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, i64, vp]),
         "vdfcg_bin_cells_indexed": (C.c_int, [vp, vp, vp, vp]),
         "vdfcg_compress_cells_indexed": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, i64, vp]),
+        "vdfcg_partition_cells": (C.c_int, [vp, i32, i32, vp]),
+        "vdfcg_multi_create": (C.c_int, [vp, i32, C.POINTER(vp)]),
+        "vdfcg_multi_destroy": (C.c_int, [vp]),
+        "vdfcg_multi_device_count": (i32, [vp]),
+        "vdfcg_multi_context": (C.c_int, [vp, i32, C.POINTER(vp)]),
+        "vdfcg_multi_compress_cells": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, i64, vp, vp]),
         "vdfcg_synth_cells": (C.c_int, [vp, i32, i32, vp, i64, u64, i32, vp, vp, vp]),
         "vdfcg_probe_peaks": (C.c_int, [vp, vp, vp]),
         "vdfcg_generate": (C.c_int, [vp, i32, i32, vp, vp, vp, i64, u64, vp, vp]),

@@ -11,7 +11,7 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libvdfcg.so")
 SOURCES = ["ctx.cu", "hist.cu", "index.cu", "em.cu", "em_d2.cu", "em_d3.cu", "em_entry.cu", "pack.cu", "synth.cu", "metrics.cu",
-           "stream.cu", "api.cu"]
+           "stream.cu", "multi.cu", "api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]

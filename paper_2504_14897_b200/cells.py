@@ -360,6 +360,70 @@ def compress_cells_indexed(batch: ParticleBatch, config: FitConfig,
     return offs, bins, results, rec, roffs
 
 
+def partition_cells(cell_offsets, n_parts: int) -> np.ndarray:
+    """Contiguous cell ranges balanced by particle count (vdfcg_partition_cells, host only):
+    part r owns cells [b[r], b[r+1])."""
+    off = np.ascontiguousarray(np.asarray(cell_offsets, dtype=np.int64))
+    out = np.zeros(n_parts + 1, dtype=np.int32)
+    _check(_api().lib().vdfcg_partition_cells(off.ctypes.data, len(off) - 1, int(n_parts), out.ctypes.data))
+    return out
+
+
+class MultiDevice:
+    """Several devices driven from this process (vdfcg_multi): one context, stream set and
+    host thread per device; cells split by particle count; records gathered in cell order."""
+
+    def __init__(self, devices):
+        api = _api()
+        self.devices = [int(x) for x in devices]
+        arr = (C.c_int32 * len(self.devices))(*self.devices)
+        h = C.c_void_p()
+        _check(api.lib().vdfcg_multi_create(arr, len(self.devices), C.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            _api().lib().vdfcg_multi_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def compress_cells(self, batch: CellBatch, config: FitConfig, meta: Optional[ModelMeta] = None,
+                       trace: bool = False, keep_bins: bool = False):
+        """compress_cells over every device (host numpy inputs). Returns
+        (bins or None, results, records, record_offsets, cell_begin)."""
+        d = batch.d
+        wm = _abi.ModelBuffers.from_model(config.warm_start) if config.warm_start is not None else None
+        cfg = _abi.fit_config_struct(config, d, wm)
+        k = max(config.initial_components, wm.k if wm else 0)
+        like = batch.axes[0]
+        bins = CellBins.alloc(batch) if keep_bins else None
+        results = CellResults(like, batch.n_cells, d, k, config.max_em_iterations if trace else 0)
+        rec = offs = None
+        cap = 0
+        ms = None
+        if meta is not None:
+            ms, _keep = _abi.meta_struct(meta, d)
+            per = 26 + 16 * d + ms.label_len + k * (1 + d + d * (d + 1) // 2) * 8
+            cap = batch.n_cells * per
+            rec = _empty(like, (max(cap, 1),), "u8")
+            offs = _empty(like, (batch.n_cells + 1,), "i64")
+        cb = np.zeros(len(self.devices) + 1, dtype=np.int32)
+        bs = bins.struct() if bins is not None else None
+        rs = results.struct()
+        _check(_api().lib().vdfcg_multi_compress_cells(
+            self.handle, C.byref(batch.struct), C.byref(cfg), C.byref(bs) if bs is not None else None,
+            C.byref(rs), C.byref(ms) if ms is not None else None, _ptr(rec), cap, _ptr(offs),
+            cb.ctypes.data))
+        if rec is not None:
+            rec = rec[:int(offs[-1])]
+        return bins, results, rec, offs, cb
+
+
 class CellMetrics:
     """Per-cell MetricsReport fields (vdfcg_cell_metrics), one array per field."""
 

@@ -14,6 +14,7 @@
 #include "em.cuh"
 #include "em_entry.cuh"
 #include "hist.cuh"
+#include "api.cuh"
 #include "metrics.cuh"
 #include "pack.cuh"
 
@@ -974,7 +975,7 @@ static bool compress_pipelined(vdfcg_ctx* ctx, const vdfcg_cells* cells,
                                const vdfcg_fit_config* cfg, const vdfcg_cell_results* warm,
                                vdfcg_cell_bins* bins, vdfcg_cell_results* out,
                                const vdfcg_model_meta* meta, uint8_t* records, int64_t capacity,
-                               int64_t* record_offsets) {
+                               int64_t* record_offsets, const EmShape& shape) {
   const int d = cells->dimension;
   if (d != 2 && d != 3) return false;
   if (cells->n_particles < (int64_t(1) << 22) || cells->n_cells < 4) return false;
@@ -1074,8 +1075,9 @@ static bool compress_pipelined(vdfcg_ctx* ctx, const vdfcg_cells* cells,
       sc.n = hoff[c1] - hoff[c0];  // this chunk's particles (histogram launch shapes)
       sc.max_cell = 0;             // known on the host: no device round trip per chunk
       for (int q = c0; q < c1; ++q) sc.max_cell = std::max(sc.max_cell, hoff[q + 1] - hoff[q]);
-      sc.shape_cells = nc;         // EM launch shape of the whole batch (bitwise-identical results)
-      sc.shape_avg = double(hoff[nc] - hoff[0]) / nc;
+      // EM launch shape of the whole batch (bitwise-identical results)
+      sc.shape_cells = shape.cells > 0 ? shape.cells : nc;
+      sc.shape_avg = shape.cells > 0 ? shape.avg : double(hoff[nc] - hoff[0]) / nc;
       launch_bin_cells(ctx, sc, sub_bins(b, c0));
       vdfcg_cell_results sw{};
       if (warm) sw = sub_warm(*warm, c0, d);
@@ -1095,18 +1097,22 @@ static bool compress_pipelined(vdfcg_ctx* ctx, const vdfcg_cells* cells,
   return true;
 }
 
-int vdfcg_compress_cells_warm(vdfcg_ctx* ctx, const vdfcg_cells* cells,
-                              const vdfcg_fit_config* cfg, const vdfcg_cell_results* warm,
-                              vdfcg_cell_bins* bins, vdfcg_cell_results* out,
-                              const vdfcg_model_meta* meta, uint8_t* records, int64_t capacity,
-                              int64_t* record_offsets) {
+}  // extern "C"
+
+namespace vdfcg {
+int compress_cells_shaped(vdfcg_ctx* ctx, const vdfcg_cells* cells, const vdfcg_fit_config* cfg,
+                          const vdfcg_cell_results* warm, vdfcg_cell_bins* bins,
+                          vdfcg_cell_results* out, const vdfcg_model_meta* meta, uint8_t* records,
+                          int64_t capacity, int64_t* record_offsets, const EmShape& shape) {
   return guard_impl([&] {
     begin(ctx);
     if (!cells) throw InvalidArgument("null cells");
     if (compress_pipelined(ctx, cells, cfg, warm, bins, out, meta, records, capacity,
-                           record_offsets))
+                           record_offsets, shape))
       return;
     CellsDev c = stage_cells(ctx, cells);
+    c.shape_cells = shape.cells;
+    c.shape_avg = shape.avg;
     validate_config(cfg, c.d);
     std::vector<std::function<void()>> fin;
     CellBinsDev b = bins_dev(ctx, c, bins, fin);
@@ -1117,6 +1123,18 @@ int vdfcg_compress_cells_warm(vdfcg_ctx* ctx, const vdfcg_cells* cells,
     for (auto& f : fin) f();
     if (any_host(fin)) sync(ctx);
   });
+}
+}  // namespace vdfcg
+
+extern "C" {
+
+int vdfcg_compress_cells_warm(vdfcg_ctx* ctx, const vdfcg_cells* cells,
+                              const vdfcg_fit_config* cfg, const vdfcg_cell_results* warm,
+                              vdfcg_cell_bins* bins, vdfcg_cell_results* out,
+                              const vdfcg_model_meta* meta, uint8_t* records, int64_t capacity,
+                              int64_t* record_offsets) {
+  return compress_cells_shaped(ctx, cells, cfg, warm, bins, out, meta, records, capacity,
+                               record_offsets, EmShape{});
 }
 
 // ---- per-particle cell-index input (index.cu) ---------------------------------------

@@ -15,8 +15,10 @@ sys.path.insert(0, ROOT)
 
 
 def _cfg():
-    return dict(workload="t", d=3, species=[("e", 6.0)], cells=24, particles=24 * 700, n_bins=24,
-                K=3, scaling="strong")
+    # skewed cells: the split must balance particles, not cells
+    counts = [300 + (c * 997) % 1400 for c in range(24)]
+    return dict(workload="t", d=3, species=[("e", 6.0)], cells=24, particles=sum(counts), n_bins=24,
+                K=3, scaling="strong", counts=counts)
 
 
 def _compress(c0, c1):
@@ -47,6 +49,28 @@ def _worker(rank, world, port, out):
     if rank == 0:
         out.put(gathered)
     dist.destroy_process_group()
+
+
+def test_partition_balances_particles():
+    """vdfcg_partition_cells (host-only): contiguous ranges covering every cell, each part's
+    particle count within one cell of total/n, identical to a numpy restatement."""
+    from paper_2504_14897_b200.cells import partition_cells
+    rng = np.random.default_rng(2)
+    for n_cells, parts in ((1000, 8), (37, 4), (5, 8), (262144, 8), (0, 3)):
+        counts = rng.integers(0, 4000, size=n_cells)
+        offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        b = partition_cells(offs, parts)
+        assert b[0] == 0 and b[-1] == n_cells and np.all(np.diff(b) >= 0)
+        total = offs[-1]
+        for r in range(1, parts):
+            t = total * r // parts
+            c = np.searchsorted(offs, t, side="left")
+            if c > 0 and (c > n_cells or t - offs[c - 1] <= offs[c] - t):
+                c -= 1
+            assert b[r] == max(c, b[r - 1]), (n_cells, parts, r)
+        if n_cells:
+            per = offs[b[1:]] - offs[b[:-1]]
+            assert per.max() - total / parts <= counts.max() + 1
 
 
 def test_two_rank_shards_cover_cells_and_match_single_process():
