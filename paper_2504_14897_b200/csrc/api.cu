@@ -3,6 +3,11 @@
 // buffers through the context stream and launches the sm_100a kernels; every number the
 // API returns is computed on the device.
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <memory>
+#include <mutex>
+#include <thread>
 #include <cmath>
 #include <cstring>
 #include <exception>
@@ -968,6 +973,108 @@ struct SideStreamGuard {
   }
 };
 
+// Pageable host inputs (a plain numpy array / Eigen matrix): cudaMemcpyAsync from pageable
+// memory blocks the calling thread, so every chunk's copy would finish before any compute is
+// enqueued. Instead host threads copy pieces of each chunk into a ring of pinned slots and
+// issue the H2D from there (truly asynchronous); a slot is reused once its previous H2D has
+// completed. The main thread records chunk j's ready event as soon as all of chunk j's
+// pieces are issued and enqueues its compute, so copy and compute overlap as for pinned input.
+class PageableStager {
+ public:
+  struct Piece {
+    const char* src;
+    char* dst;
+    size_t bytes;
+    int chunk;
+  };
+  PageableStager(vdfcg_ctx* ctx, std::vector<Piece> pieces, int n_chunks)
+      : ctx_(ctx), pieces_(std::move(pieces)), issued_(pieces_.size()), left_(n_chunks, 0) {
+    constexpr size_t kSlot = size_t(64) << 20;
+    constexpr int kSlots = 12;
+    if (!ctx->ring) {
+      VDFCG_CUDA(cudaHostAlloc(&ctx->ring, kSlot * kSlots, cudaHostAllocDefault));
+      ctx->ring_slot = kSlot;
+      ctx->ring_slots = kSlots;
+      ctx->ring_ev.resize(kSlots);
+      for (auto& e : ctx->ring_ev) VDFCG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    for (auto& f : issued_) f.store(false);
+    for (const auto& p : pieces_) ++left_[p.chunk];
+    const int threads = std::min<int>(6, std::max<int>(1, static_cast<int>(pieces_.size())));
+    for (int t = 0; t < threads; ++t) th_.emplace_back([this] { run(); });
+  }
+  ~PageableStager() {
+    for (auto& t : th_) t.join();
+  }
+  // Blocks until every piece of chunk j has been issued on the copy stream.
+  void wait_chunk(int j) {
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_.wait(lk, [&] { return left_[j] == 0 || failed_; });
+    if (failed_) throw CudaError(err_);
+  }
+  static size_t slot_bytes() { return size_t(64) << 20; }
+
+ private:
+  void run() {
+    cudaSetDevice(ctx_->device);
+    for (;;) {
+      const size_t i = next_.fetch_add(1);
+      if (i >= pieces_.size() || failed_) return;
+      const int slots = ctx_->ring_slots;
+      const int slot = static_cast<int>(i % slots);
+      // the slot's previous piece must have been issued (its event recorded) and copied
+      if (i >= size_t(slots)) {
+        while (!issued_[i - slots].load(std::memory_order_acquire)) std::this_thread::yield();
+        if (cudaEventSynchronize(ctx_->ring_ev[slot]) != cudaSuccess) return fail("staging H2D failed");
+      }
+      char* buf = static_cast<char*>(ctx_->ring) + size_t(slot) * ctx_->ring_slot;
+      const Piece& p = pieces_[i];
+      std::memcpy(buf, p.src, p.bytes);
+      {
+        // one issuer at a time: the H2D and its slot event go onto the copy stream in order
+        std::lock_guard<std::mutex> lk(issue_mu_);
+        if (cudaMemcpyAsync(p.dst, buf, p.bytes, cudaMemcpyHostToDevice, ctx_->copy_stream) != cudaSuccess ||
+            cudaEventRecord(ctx_->ring_ev[slot], ctx_->copy_stream) != cudaSuccess)
+          return fail("staging H2D failed");
+      }
+      issued_[i].store(true, std::memory_order_release);
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        --left_[p.chunk];
+      }
+      cv_.notify_all();
+    }
+  }
+  void fail(const char* msg) {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      failed_ = true;
+      err_ = msg;
+    }
+    cv_.notify_all();
+  }
+  vdfcg_ctx* ctx_;
+  std::vector<Piece> pieces_;
+  std::vector<std::atomic<bool>> issued_;
+  std::vector<int> left_;
+  std::atomic<size_t> next_{0};
+  std::mutex mu_, issue_mu_;
+  std::condition_variable cv_;
+  std::atomic<bool> failed_{false};
+  std::string err_;
+  std::vector<std::thread> th_;
+};
+
+static bool pageable_host(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
 // Host-resident particles: the velocity (and weight) ranges of successive cell chunks are
 // copied on the context's copy stream while the compute stream bins and fits the chunks
 // already resident, so the end-to-end time approaches max(H2D, compute) instead of the sum.
@@ -1031,6 +1138,7 @@ static bool compress_pipelined(vdfcg_ctx* ctx, const vdfcg_cells* cells,
     bounds.push_back(std::max(bounds.back(), std::min(cb, nc)));
   }
   bounds.push_back(nc);
+  validate_config(cfg, d);
   // the copy stream starts after everything already queued on the compute stream
   EventPool events;
   SideStreamGuard side{ctx};
@@ -1039,20 +1147,40 @@ static bool compress_pipelined(vdfcg_ctx* ctx, const vdfcg_cells* cells,
   VDFCG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, start, 0));
   std::vector<cudaEvent_t> ready(bounds.size() - 1);
   for (auto& e : ready) e = events.make();
-  for (size_t j = 0; j + 1 < bounds.size(); ++j) {
-    const int64_t p0 = hoff[bounds[j]], p1 = hoff[bounds[j + 1]];
-    const size_t bytes = size_t(p1 - p0) * sizeof(double);
-    if (bytes) {
-      for (int a = 0; a < d; ++a)
-        VDFCG_CUDA(cudaMemcpyAsync(dv[a] + p0, cells->velocity[a] + p0, bytes,
-                                   cudaMemcpyHostToDevice, ctx->copy_stream));
-      if (dw)
-        VDFCG_CUDA(cudaMemcpyAsync(dw + p0, cells->weights + p0, bytes, cudaMemcpyHostToDevice,
-                                   ctx->copy_stream));
+  bool pageable = cells->weights && pageable_host(cells->weights);
+  for (int a = 0; a < d; ++a) pageable = pageable || pageable_host(cells->velocity[a]);
+  std::unique_ptr<PageableStager> stager;
+  if (pageable) {
+    std::vector<PageableStager::Piece> pieces;
+    const size_t slot = PageableStager::slot_bytes();
+    for (size_t j = 0; j + 1 < bounds.size(); ++j) {
+      const int64_t p0 = hoff[bounds[j]], p1 = hoff[bounds[j + 1]];
+      const size_t bytes = size_t(p1 - p0) * sizeof(double);
+      for (int a = 0; a <= d; ++a) {
+        const double* src = a < d ? cells->velocity[a] : cells->weights;
+        double* dst = a < d ? dv[a] : dw;
+        if (!src) continue;
+        for (size_t o = 0; o < bytes; o += slot)
+          pieces.push_back({reinterpret_cast<const char*>(src + p0) + o, reinterpret_cast<char*>(dst + p0) + o,
+                            std::min(slot, bytes - o), static_cast<int>(j)});
+      }
     }
-    VDFCG_CUDA(cudaEventRecord(ready[j], ctx->copy_stream));
+    stager = std::make_unique<PageableStager>(ctx, std::move(pieces), static_cast<int>(ready.size()));
+  } else {
+    for (size_t j = 0; j + 1 < bounds.size(); ++j) {
+      const int64_t p0 = hoff[bounds[j]], p1 = hoff[bounds[j + 1]];
+      const size_t bytes = size_t(p1 - p0) * sizeof(double);
+      if (bytes) {
+        for (int a = 0; a < d; ++a)
+          VDFCG_CUDA(cudaMemcpyAsync(dv[a] + p0, cells->velocity[a] + p0, bytes,
+                                     cudaMemcpyHostToDevice, ctx->copy_stream));
+        if (dw)
+          VDFCG_CUDA(cudaMemcpyAsync(dw + p0, cells->weights + p0, bytes, cudaMemcpyHostToDevice,
+                                     ctx->copy_stream));
+      }
+      VDFCG_CUDA(cudaEventRecord(ready[j], ctx->copy_stream));
+    }
   }
-  validate_config(cfg, d);
   std::vector<std::function<void()>> fin;
   CellBinsDev b = bins_dev(ctx, c, bins, fin);
   EmOut o = results_dev(ctx, nc, d, out, fin);
@@ -1070,6 +1198,10 @@ static bool compress_pipelined(vdfcg_ctx* ctx, const vdfcg_cells* cells,
       const int c0 = bounds[j], c1 = bounds[j + 1];
       if (c1 <= c0) continue;
       ctx->stream = (j & 1) ? ctx->aux_stream : main;
+      if (stager) {  // pageable input: chunk j's pieces issued -> its ready event
+        stager->wait_chunk(static_cast<int>(j));
+        VDFCG_CUDA(cudaEventRecord(ready[j], ctx->copy_stream));
+      }
       VDFCG_CUDA(cudaStreamWaitEvent(ctx->stream, ready[j], 0));
       CellsDev sc = sub_cells(c, c0, c1);
       sc.n = hoff[c1] - hoff[c0];  // this chunk's particles (histogram launch shapes)

@@ -179,6 +179,8 @@ int vdfcg_ctx_destroy(vdfcg_ctx* ctx) {
       cudaStreamSynchronize(ctx->copy_stream);
       cudaStreamDestroy(ctx->copy_stream);
     }
+    for (auto e : ctx->ring_ev) cudaEventDestroy(e);
+    if (ctx->ring) cudaFreeHost(ctx->ring);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     if (ctx->handoff) cudaEventDestroy(ctx->handoff);
     delete ctx;

@@ -55,6 +55,11 @@ struct vdfcg_ctx {
   std::vector<Chunk> chunks;
   // pinned scalar readback slot
   void* pinned = nullptr;
+  // pinned staging ring for pageable host inputs (allocated on first use)
+  void* ring = nullptr;
+  size_t ring_slot = 0;
+  int ring_slots = 0;
+  std::vector<cudaEvent_t> ring_ev;
   // device diagnostics counters: [0] exact second EM passes run
   unsigned long long* diag = nullptr;
   // timing

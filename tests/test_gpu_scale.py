@@ -274,6 +274,34 @@ def test_pipelined_host_path_weighted_bitwise():
     assert torch.equal(rd.weights.cpu().view(torch.int64), rh.weights.view(torch.int64))
 
 
+@pytest.mark.parametrize("weighted", [False, True])
+def test_pageable_host_path_bitwise_equals_device_path(weighted):
+    """Pageable host inputs (plain numpy, as a reference caller's Eigen storage) go through
+    the pinned staging ring (host copy threads + async H2D) and must give the device path's
+    results bit for bit; small 64 MB staging slots mean many pieces per chunk."""
+    import torch
+    dev = torch.device("cuda", 0)
+    n_cells, per = 3000, 1700
+    offs = torch.arange(n_cells + 1, dtype=torch.int64, device=dev) * per
+    axes = [torch.empty(n_cells * per, dtype=torch.float64, device=dev) for _ in range(3)]
+    G.synth_cells(3, offs, 23, 0, *axes)
+    w = None
+    if weighted:
+        w = torch.rand(n_cells * per, dtype=torch.float64, device=dev,
+                       generator=torch.Generator(dev).manual_seed(5)) * 3.0 + 0.1
+    cfg = FitConfig(initial_components=4, seed=7, temperature=np.ones(3))
+    meta = ModelMeta("e", None, 4, [AxisRange(-6, 6)] * 3)
+    _, rd, recd, offd = G.compress_cells(G.CellBatch(axes, offs, 48, [-6] * 3, [6] * 3, w), cfg, meta)
+    hv = [np.ascontiguousarray(a.cpu().numpy()) for a in axes]  # pageable
+    hw = None if w is None else np.ascontiguousarray(w.cpu().numpy())
+    hb = G.CellBatch(hv, offs.cpu().numpy(), 48, [-6] * 3, [6] * 3, hw)
+    assert hb.n >= (1 << 22)
+    _, rh, rech, offh = G.compress_cells(hb, cfg, meta)
+    assert bytes(recd.cpu().numpy()) == bytes(rech) and np.array_equal(offd.cpu().numpy(), offh)
+    for f in ("status", "components", "iterations", "final_loglik"):
+        assert np.array_equal(getattr(rd, f).cpu().numpy(), getattr(rh, f)), f
+
+
 def test_cfg3_full_size_parity():
     """BASELINE cfg3 at full size: 16x16 cells x 390625 particles (1e8), 3V 32^3 bins, K=3
     (the reference's per-part fit_one_plane, pipeline.cpp:130-160, on every cell). Every
