@@ -4,8 +4,11 @@
 //    particle columns (all three marginals from one read for all_planes), per-CTA
 //    shared-memory privatised u32 counters (unit weights: exact integers) merged into
 //    global memory with one atomic per non-empty bin, out-of-range mass per CTA.
+//    Fractional weights: per-particle bin -> stable device group-by (index.cu) -> every
+//    bin summed sequentially in particle order = the reference's `+=`, bit for bit.
 // K2 cells_dense: per-cell bins^d histograms for cells much larger than the grid
-//    (SURVEY.md App. A), work items = (cell, chunk), shared-memory privatised counters.
+//    (SURVEY.md App. A), work items = (cell, chunk), shared-memory privatised counters;
+//    fractional weights take the ordered composite-id path (cells_weighted_ordered).
 // K3 cells_sort: per-cell sort of composite (bin, particle) keys for cells much
 //    smaller than the grid (48^3, 64^3): the sorted runs ARE the compacted histogram in
 //    ascending bin order (= to_weighted_points(drop_empty) order), and fractional
@@ -141,6 +144,72 @@ static void hist2d_dispatch(vdfcg_ctx* ctx, int grid, int block, size_t smem, co
                                                                      goor, goorw, err));
 }
 
+// Weighted bin_particles / all_planes in the reference's summation order: every bin (and the
+// out-of-range total) is the sequential sum `counts(i,j) += w` over the particles in input
+// order (histogram.cpp:66-74). Per plane: each particle's column-major bin (or n^2 for out
+// of range) -> the stable device group-by (index.cu) puts every bin's weights contiguous in
+// particle order -> one thread per bin adds them in that order from 0.0. Bit-identical to
+// the reference and run-to-run deterministic (the atomic scatter is neither).
+__global__ void plane_bin_kernel(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
+                                 int nb, double xlo, double xhi, double ylo, double yhi, double invx,
+                                 double invy, int32_t* __restrict__ bin) {
+  const int32_t oor = nb * nb;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int bi = bin_index(__ldg(x + i), xlo, xhi, nb, invx);
+    const int bj = bin_index(__ldg(y + i), ylo, yhi, nb, invy);
+    bin[i] = (bi < 0 || bj < 0) ? oor : bi + bj * nb;  // column-major counts(i, j)
+  }
+}
+
+__global__ void ordered_bin_sum_kernel(const double* __restrict__ wg, const int64_t* __restrict__ off,
+                                       int32_t nn, double* __restrict__ counts, double* __restrict__ oor) {
+  for (int32_t b = blockIdx.x * blockDim.x + threadIdx.x; b <= nn; b += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t p = off[b]; p < off[b + 1]; ++p) s = __dadd_rn(s, __ldg(wg + p));
+    if (b < nn) counts[b] = s;
+    else *oor = s;
+  }
+}
+
+static void hist2d_weighted_ordered(vdfcg_ctx* ctx, const double* vel, int64_t n, const double* w, int nplanes,
+                                    const int* ax, const int* ay, int n_bins, const double* xlo,
+                                    const double* xhi, const double* ylo, const double* yhi,
+                                    double* counts_out, double* oor_out, int* err) {
+  const int32_t nn = n_bins * n_bins;
+  int32_t* bin = arena<int32_t>(ctx, size_t(std::max<int64_t>(n, 1)));
+  uint32_t* keys = arena<uint32_t>(ctx, size_t(std::max<int64_t>(n, 1)));
+  double* wg = arena<double>(ctx, size_t(std::max<int64_t>(n, 1)));
+  int64_t* off = arena<int64_t>(ctx, size_t(nn) + 2);
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, int64_t(ctx->sm_count) * 8)));
+  for (int q = 0; q < nplanes; ++q) {
+    const double* x = vel + static_cast<int64_t>(ax[q]) * n;
+    const double* y = vel + static_cast<int64_t>(ay[q]) * n;
+    if (n > 0)
+      VDFCG_LAUNCH(ctx, "hist2d_bin",
+                   plane_bin_kernel<<<grid, 256, 0, ctx->stream>>>(x, y, n, n_bins, xlo[q], xhi[q], ylo[q], yhi[q],
+                                                                   n_bins / (xhi[q] - xlo[q]),
+                                                                   n_bins / (yhi[q] - ylo[q]), bin));
+    IndexedDev in{};
+    in.d = 2;
+    in.n = n;
+    in.vel[0] = x;
+    in.vel[1] = y;
+    in.vel[2] = x;
+    in.w = w;
+    in.cell = bin;
+    in.n_cells = nn + 1;  // + the out-of-range bin
+    in.n_bins = 2;
+    in.lo[0] = in.lo[1] = in.lo[2] = 0.0;
+    in.hi[0] = in.hi[1] = in.hi[2] = 1.0;
+    launch_group_cells(ctx, in, GroupedDev{keys, wg, off}, err);
+    const int g2 = std::max(1, std::min((nn + 256) / 256, ctx->sm_count * 8));
+    VDFCG_LAUNCH(ctx, "hist2d_ordered_sum",
+                 ordered_bin_sum_kernel<<<g2, 256, 0, ctx->stream>>>(wg, off, nn, counts_out + size_t(q) * nn,
+                                                                   oor_out + q));
+  }
+}
+
 void launch_hist2d(vdfcg_ctx* ctx, const double* vel, int64_t n, int d, const double* w,
                    int nplanes, const int* ax, const int* ay, int n_bins, const double* xlo,
                    const double* xhi, const double* ylo, const double* yhi, double* counts_out,
@@ -165,6 +234,15 @@ void launch_hist2d(vdfcg_ctx* ctx, const double* vel, int64_t n, int d, const do
   const bool use_smem = smem <= 112 * 1024;
   int* err = arena<int>(ctx, 1);
   VDFCG_CUDA(cudaMemsetAsync(err, 0, sizeof(int), ctx->stream));
+  if (weighted) {  // reference summation order (bit-exact), see hist2d_weighted_ordered
+    hist2d_weighted_ordered(ctx, vel, n, w, nplanes, ax, ay, n_bins, xlo, xhi, ylo, yhi, counts_out,
+                            oor_out, err);
+    int* h = static_cast<int*>(ctx->pinned);
+    VDFCG_CUDA(cudaMemcpyAsync(h, err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    if (*h & 2) throw InvalidArgument("particle weights must all be > 0");
+    return;
+  }
   unsigned* gcnt = nullptr;
   unsigned long long* goor = nullptr;
   if (weighted) {
@@ -956,6 +1034,76 @@ static bool try_sort_path(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& 
   return true;
 }
 
+// Weighted cells too large for the per-cell sort (> 8192 particles): every (cell, bin) sum
+// in particle order (histogram.cpp:66-74) through the stable device group-by over the
+// composite id c * (bins + 1) + bin (bins = the cell's out-of-range slot); then one thread
+// per id adds its weights sequentially into the dense per-cell grid the compaction reads.
+__global__ void fill_i32_kernel(int32_t* p, int64_t n, int32_t v) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+
+template <int D>
+__global__ void cell_composite_kernel(VelPtrs vp, const int64_t* __restrict__ offsets, int n_cells,
+                                      CellGeom g, int64_t bins, int32_t* __restrict__ ids) {
+  for (int c = blockIdx.x; c < n_cells; c += gridDim.x) {
+    const int64_t b = offsets[c], e = offsets[c + 1];
+    const int64_t base = static_cast<int64_t>(c) * (bins + 1);
+    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+      const int64_t key = cell_key<D>(vp, i, g);
+      ids[i] = static_cast<int32_t>(base + (key < 0 ? bins : key));
+    }
+  }
+}
+
+__global__ void composite_sum_kernel(const double* __restrict__ wg, const int64_t* __restrict__ off,
+                                     int64_t n_ids, int64_t bins, double* __restrict__ densew,
+                                     double* __restrict__ oorw) {
+  for (int64_t id = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; id < n_ids;
+       id += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t p0 = off[id], p1 = off[id + 1];
+    double s = 0.0;
+    for (int64_t p = p0; p < p1; ++p) s = __dadd_rn(s, __ldg(wg + p));
+    const int64_t c = id / (bins + 1), k = id - c * (bins + 1);
+    if (k == bins) oorw[c] = s;
+    else densew[c * bins + k] = s;
+  }
+}
+
+template <int D>
+static void cells_weighted_ordered(vdfcg_ctx* ctx, const CellsDev& c, const CellGeom& g, int64_t bins,
+                                   double* densew, double* oorw, int* err) {
+  const int64_t n_ids = int64_t(c.n_cells) * (bins + 1);
+  const int64_t n = std::max<int64_t>(c.n, 1);
+  int32_t* ids = arena<int32_t>(ctx, size_t(n));
+  uint32_t* keys = arena<uint32_t>(ctx, size_t(n));
+  double* wg = arena<double>(ctx, size_t(n));
+  int64_t* off = arena<int64_t>(ctx, size_t(n_ids) + 2);
+  const int g1 = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, int64_t(ctx->sm_count) * 8)));
+  // particles outside every cell range get the extra id n_ids (grouped, never summed)
+  VDFCG_LAUNCH(ctx, "cells_ordered_ids",
+               fill_i32_kernel<<<g1, 256, 0, ctx->stream>>>(ids, c.n, static_cast<int32_t>(n_ids)));
+  VelPtrs vp{{c.vel[0], c.vel[1], c.vel[2]}, c.keys};
+  const int gc = std::max(1, std::min(c.n_cells, ctx->sm_count * 8));
+  VDFCG_LAUNCH(ctx, "cells_ordered_ids",
+               cell_composite_kernel<D><<<gc, 512, 0, ctx->stream>>>(vp, c.offsets, c.n_cells, g, bins, ids));
+  IndexedDev in{};
+  in.d = 2;
+  in.n = c.n;
+  in.vel[0] = in.vel[1] = in.vel[2] = c.w;  // read-only dummy: the group keys are not used
+  in.w = c.w;
+  in.cell = ids;
+  in.n_cells = static_cast<int>(n_ids + 1);
+  in.n_bins = 2;
+  in.lo[0] = in.lo[1] = in.lo[2] = 0.0;
+  in.hi[0] = in.hi[1] = in.hi[2] = 1.0;
+  launch_group_cells(ctx, in, GroupedDev{keys, wg, off}, err);
+  const int g2 = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n_ids + 255) / 256, int64_t(ctx->sm_count) * 16)));
+  VDFCG_LAUNCH(ctx, "cells_ordered_sum",
+               composite_sum_kernel<<<g2, 256, 0, ctx->stream>>>(wg, off, n_ids, bins, densew, oorw));
+}
+
 // D = velocity axes read by the kernels, or 0 when the bin keys were computed upstream
 // (c.keys, the cell-index path); the grid dimension is c.d either way.
 template <int D>
@@ -1075,6 +1223,11 @@ static void bin_cells_d(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
       VDFCG_CUDA(cudaMemsetAsync(dense, 0, total_bins * 4, ctx->stream));
       VDFCG_CUDA(cudaMemsetAsync(oor_cnt, 0, c.n_cells * 8, ctx->stream));
     }
+    const bool ordered = weighted && int64_t(c.n_cells) * (bins + 1) + 1 < (int64_t(1) << 31) &&
+                         c.n < (int64_t(1) << 32);
+    if (ordered) {  // reference summation order (bit-exact), see cells_weighted_ordered
+      cells_weighted_ordered<D>(ctx, c, g, bins, densew, oorw, err);
+    } else {
     const bool smem_ok = !weighted && bins * 4 <= 160 * 1024;
     const int block = 1024;
     // chunk: enough items to fill every SM several times, >= 16K particles each
@@ -1107,6 +1260,7 @@ static void bin_cells_d(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
                    k<<<grid, block, 0, ctx->stream>>>(vp, c.w, c.offsets, c.n_cells, item_off,
                                                       chunk, g, bins, dense, densew, oor_cnt, oorw,
                                                       err));
+    }
     }
     const int grid = std::max(1, std::min(c.n_cells, ctx->sm_count * 4));
     if (weighted)

@@ -51,8 +51,30 @@ def test_bin_particles_weighted_and_edges():
     p = ParticleSet(v, w, "x", np.ones(2))
     hg = G.bin_particles(p, Plane.uv, 50, AxisRange(-1, 1), AxisRange(-1, 1))
     ho = O.bin_particles(p, Plane.uv, 50, AxisRange(-1, 1), AxisRange(-1, 1))
-    np.testing.assert_allclose(hg.counts, ho.counts, rtol=TOL_WEIGHTED_HIST, atol=0)
-    assert rel(hg.out_of_range_count, ho.out_of_range_count) <= TOL_WEIGHTED_HIST
+    # every bin summed in particle order, like the reference's sequential `+=`: bit-exact
+    assert np.array_equal(hg.counts, ho.counts)
+    assert hg.out_of_range_count == ho.out_of_range_count
+
+
+@pytest.mark.parametrize("n,nb", [(1_000_000, 64), (300_000, 200), (50_000, 2)])
+def test_weighted_bin_particles_and_all_planes_bit_exact(n, nb):
+    """Fractional weights (w ~ U(0.1, 4), test_histogram.cpp:76): bit-identical to the
+    reference's sequential sums for bin_particles and all_planes, and run-to-run stable."""
+    rng = np.random.default_rng(n + nb)
+    v = rng.normal(size=(n, 3)) * 1.7
+    w = rng.uniform(0.1, 4.0, size=n)
+    p = ParticleSet(v, w, "x", np.ones(3))
+    hg = G.bin_particles(p, Plane.vw, nb, AxisRange(-4, 4), AxisRange(-4, 4))
+    ho = O.bin_particles(p, Plane.vw, nb, AxisRange(-4, 4), AxisRange(-4, 4))
+    assert np.array_equal(hg.counts, ho.counts)
+    assert hg.out_of_range_count == ho.out_of_range_count
+    ag = G.all_planes(p, nb, AxisRange(-4, 4))
+    ao = O.all_planes(p, nb, AxisRange(-4, 4))
+    for a, b in zip(ag, ao):
+        assert np.array_equal(a.counts, b.counts)
+        assert a.out_of_range_count == b.out_of_range_count
+    again = G.all_planes(p, nb, AxisRange(-4, 4))
+    assert all(np.array_equal(a.counts, b.counts) for a, b in zip(ag, again))
 
 
 def test_all_planes_bit_exact():
@@ -222,3 +244,20 @@ def test_bin_cells_staging_edges(misaligned):
         assert np.array_equal(keys[b:b + k], ob.keys[b:b + k])
         assert np.array_equal(cnts[b:b + k], ob.counts[b:b + k])
     assert np.array_equal(gb.out_of_range.cpu().numpy(), ob.out_of_range)
+
+
+def test_weighted_dense_cells_bit_exact():
+    """Weighted cells larger than the per-cell sort (> 8192 particles: cfg3-like dense cells)
+    take the ordered composite-id path: every (cell, bin) summed in particle order — equal
+    to the oracle's sequential sums bit for bit; in_range (Eigen sum()) within 1e-12."""
+    v, offs, w, lo, hi = _cells_case(3, 6, 40_000, 32, seed=4, weighted=True)
+    from paper_2504_14897_b200 import cells as GC
+    gb = GC.bin_cells(GC.CellBatch(v, offs, 32, lo, hi, weights=w))
+    ob = O.bin_cells(O.CellsHost(v, offs, 32, lo, hi, w))
+    assert np.array_equal(gb.nnz, ob.nnz)
+    assert np.array_equal(gb.out_of_range, ob.out_of_range)
+    np.testing.assert_allclose(gb.in_range, ob.in_range, rtol=TOL_WEIGHTED_HIST)
+    for c in range(len(offs) - 1):
+        b, k = offs[c], ob.nnz[c]
+        assert np.array_equal(gb.keys[b:b + k], ob.keys[b:b + k]), c
+        assert np.array_equal(gb.counts[b:b + k], ob.counts[b:b + k]), c
