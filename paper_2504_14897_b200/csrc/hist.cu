@@ -313,13 +313,20 @@ __global__ void __launch_bounds__(1024) twp_kernel(const double* __restrict__ co
   // Pass 1: count kept bins; in-range total summed in column-major storage order by
   // one thread (Histogram2D::in_range_count, histogram.hpp:25).
   long long kept = 0;
-  for (int64_t f = threadIdx.x; f < nn; f += blockDim.x) kept += (counts[f] > 0.0) ? 1 : 0;
+  double part = 0.0;
+  for (int64_t f = threadIdx.x; f < nn; f += blockDim.x) {
+    const double c = counts[f];
+    kept += (c > 0.0) ? 1 : 0;
+    part += c;
+  }
   long long tot_kept = Reduce(rs).Sum(kept);
+  // in_range_count (Eigen sum(), histogram.hpp:25) in a fixed tree order: exact for integer
+  // counts, deterministic for fractional ones
+  __shared__ typename cub::BlockReduce<double, 1024>::TempStorage rds;
+  const double total = cub::BlockReduce<double, 1024>(rds).Sum(part);
   if (threadIdx.x == 0) {
     s_kept = drop_empty ? tot_kept : nn;
-    double t = 0.0;
-    for (int64_t f = 0; f < nn; ++f) t += counts[f];
-    *total_out = t;
+    *total_out = total;
     *count_out = s_kept;
     s_run = 0;
   }
@@ -957,21 +964,36 @@ __global__ void chunks_per_cell_kernel(const int64_t* offsets, int n_cells, int6
   }
 }
 
+// Exclusive scan of n int64 values, total at out[n]: one CTA walking 4096-element tiles with
+// coalesced loads and a running prefix (n = cells of a batch).
 __global__ void __launch_bounds__(1024) scan_i64_kernel(const int64_t* in, int64_t* out, int64_t n) {
   using Scan = cub::BlockScan<long long, 1024>;
   __shared__ typename Scan::TempStorage ss;
-  const int64_t seg = (n + 1023) / 1024;
-  const int64_t s = threadIdx.x * seg, e = min(n, s + seg);
-  long long local = 0;
-  for (int64_t i = s; i < e; ++i) local += in[i];
-  long long pre, tot;
-  Scan(ss).ExclusiveSum(local, pre, tot);
-  for (int64_t i = s; i < e; ++i) {
-    const long long v = in[i];
-    out[i] = pre;
-    pre += v;
+  __shared__ long long s_run;
+  if (threadIdx.x == 0) s_run = 0;
+  __syncthreads();
+  for (int64_t t0 = 0; t0 < n; t0 += 4096) {
+    long long x[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t k = t0 + threadIdx.x + i * 1024;  // coalesced
+      x[i] = k < n ? in[k] : 0;
+    }
+    // thread t owns elements t, t+1024, ...: four block scans in (i, t) order
+    long long run = s_run;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      long long pre, tot;
+      Scan(ss).ExclusiveSum(x[i], pre, tot);
+      const int64_t k = t0 + threadIdx.x + i * 1024;
+      if (k < n) out[k] = run + pre;
+      run += tot;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) s_run = run;
+    __syncthreads();
   }
-  if (threadIdx.x == 0) out[n] = tot;
+  if (threadIdx.x == 0) out[n] = s_run;
 }
 
 void launch_scan_i64(vdfcg_ctx* ctx, const int64_t* in, int64_t* out, int64_t n) {
