@@ -794,6 +794,43 @@ struct Stage {
   static constexpr int kA = 16 / kElem;
 };
 
+// Every array 16-byte aligned (sh == 0): the window starts at the even (D > 0) / 4-aligned
+// (keys) element at or below b; only an element past lim-1 at the very end is loaded directly.
+template <int D>
+VDFCG_DEV void issue_cell_copy_aligned(const VelPtrs& vp, const int64_t* offsets, int c, int64_t lim,
+                                       unsigned char* pbuf, int capp, uint64_t* bar) {
+  using S = Stage<D>;
+  constexpr int A = S::kA;
+  const int64_t b = offsets[c], e = offsets[c + 1];
+  const int64_t b0 = b & ~int64_t(A - 1);
+  int64_t e0 = (e + A - 1) & ~int64_t(A - 1);
+  int64_t ed = e0;  // directly loaded tail [ed, e)
+  if (e0 > lim) {
+    e0 -= A;
+    ed = e0;
+  }
+  const uint32_t bytes = e0 > b0 ? static_cast<uint32_t>((e0 - b0) * S::kElem) : 0u;
+  for (int64_t x = ed; x < e; ++x) {
+#pragma unroll
+    for (int a = 0; a < S::kArrays; ++a) {
+      if constexpr (D == 0)
+        reinterpret_cast<uint32_t*>(pbuf)[x - b0] = __ldg(vp.keys + x);
+      else
+        reinterpret_cast<double*>(pbuf)[a * capp + (x - b0)] = __ldg(vp.v[a] + x);
+    }
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  bar_expect(bar, bytes * S::kArrays);
+  if (bytes)
+#pragma unroll
+    for (int a = 0; a < S::kArrays; ++a) {
+      if constexpr (D == 0)
+        bulk_g2s(reinterpret_cast<uint32_t*>(pbuf), vp.keys + b0, bytes, bar);
+      else
+        bulk_g2s(reinterpret_cast<double*>(pbuf) + a * capp, vp.v[a] + b0, bytes, bar);
+    }
+}
+
 template <int D>
 VDFCG_DEV void issue_cell_copy(const VelPtrs& vp, const int64_t* offsets, int c, int64_t lim,
                                unsigned char* pbuf, int capp, const int* sh, uint64_t* bar) {
@@ -839,8 +876,11 @@ struct StageShift {
   int sh[3];
 };
 
-template <int D, int BLOCK, int kTmaWpt>  // kTmaWpt >= bitmap words per thread
-__global__ void __launch_bounds__(BLOCK) cells_bitmap_tma_kernel(
+template <int D, int BLOCK, int kTmaWpt, bool GEN, int MINB>  // kTmaWpt >= bitmap words per
+// thread; GEN: some array base is not 16-byte aligned (per-array skew), else the aligned
+// fast form; MINB: CTAs per SM the shared memory allows (3 caps registers at 40 for 512
+// threads: small bitmaps run three CTAs, larger ones two with more registers)
+__global__ void __launch_bounds__(BLOCK) __maxnreg__(MINB == 3 ? 40 : 48) cells_bitmap_tma_kernel(
     VelPtrs vp, const int64_t* __restrict__ offsets, int n_cells, CellGeom g, int words, int ccap,
     int capp, StageShift ss_, int32_t* nnz, uint32_t* __restrict__ keys_out,
     double* __restrict__ counts_out, double* oor_out, double* in_range) {
@@ -864,7 +904,10 @@ __global__ void __launch_bounds__(BLOCK) cells_bitmap_tma_kernel(
     s_oor = 0u;
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (blockIdx.x < n_cells) issue_cell_copy<D>(vp, offsets, blockIdx.x, lim, pbuf, capp, ss_.sh, &bar);
+    if (blockIdx.x < n_cells) {
+      if constexpr (GEN) issue_cell_copy<D>(vp, offsets, blockIdx.x, lim, pbuf, capp, ss_.sh, &bar);
+      else issue_cell_copy_aligned<D>(vp, offsets, blockIdx.x, lim, pbuf, capp, &bar);
+    }
   }
   __syncthreads();
   uint32_t parity = 0;
@@ -873,7 +916,8 @@ __global__ void __launch_bounds__(BLOCK) cells_bitmap_tma_kernel(
     const int nc = static_cast<int>(offsets[c + 1] - b);
     int skew[S::kArrays];
 #pragma unroll
-    for (int a = 0; a < S::kArrays; ++a) skew[a] = static_cast<int>((b + ss_.sh[a]) % S::kA);
+    for (int a = 0; a < S::kArrays; ++a)
+      skew[a] = GEN ? static_cast<int>((b + ss_.sh[a]) % S::kA) : static_cast<int>(b & (S::kA - 1));
     bar_wait(&bar, parity);
     parity ^= 1u;
     // 1. occupancy bits from the staged slices
@@ -907,7 +951,10 @@ __global__ void __launch_bounds__(BLOCK) cells_bitmap_tma_kernel(
     __syncthreads();
     // the staging buffer is free: fetch the next cell while this one is ranked
     if (threadIdx.x == 0 && c + static_cast<int>(gridDim.x) < n_cells)
-      issue_cell_copy<D>(vp, offsets, c + gridDim.x, lim, pbuf, capp, ss_.sh, &bar);
+    {
+      if constexpr (GEN) issue_cell_copy<D>(vp, offsets, c + gridDim.x, lim, pbuf, capp, ss_.sh, &bar);
+      else issue_cell_copy_aligned<D>(vp, offsets, c + gridDim.x, lim, pbuf, capp, &bar);
+    }
     // 2. ranks; the word popcounts stay in registers for the prefix and the re-zeroing
     unsigned local = 0, pc[kTmaWpt];
 #pragma unroll
@@ -1195,8 +1242,23 @@ static void bin_cells_d(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
   }
   if (!weighted && tma_fits && choice == 1) {
     const bool w8 = words <= 8 * tb;
-    auto k = tb == 512 ? (w8 ? cells_bitmap_tma_kernel<D, 512, 8> : cells_bitmap_tma_kernel<D, 512, 16>)
-                       : (w8 ? cells_bitmap_tma_kernel<D, 256, 8> : cells_bitmap_tma_kernel<D, 256, 16>);
+    bool gen = false;
+    for (int a = 0; a < S::kArrays; ++a) gen = gen || shift.sh[a] != 0;
+    const bool three = tma_smem * 3 + 3 * 1024 <= 227 * 1024;
+    using KFn = void (*)(VelPtrs, const int64_t*, int, CellGeom, int, int, int, StageShift, int32_t*,
+                         uint32_t*, double*, double*, double*);
+    KFn k;
+#define VDFCG_TMA_PICK(B, WPT)                                                                     \
+  k = gen ? (three ? cells_bitmap_tma_kernel<D, B, WPT, true, 3> : cells_bitmap_tma_kernel<D, B, WPT, true, 1>) \
+          : (three ? cells_bitmap_tma_kernel<D, B, WPT, false, 3> : cells_bitmap_tma_kernel<D, B, WPT, false, 1>)
+    if (tb == 512) {
+      if (w8) VDFCG_TMA_PICK(512, 8);
+      else VDFCG_TMA_PICK(512, 16);
+    } else {
+      if (w8) VDFCG_TMA_PICK(256, 8);
+      else VDFCG_TMA_PICK(256, 16);
+    }
+#undef VDFCG_TMA_PICK
     VDFCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tma_smem)));
     int occ = 0;
     VDFCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, tb, tma_smem));
