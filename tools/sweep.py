@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--cells", type=int, default=65536)
     ap.add_argument("--per", type=int, default=1907)
     ap.add_argument("--json", default=None)
+    ap.add_argument("--cpu-cells", type=int, default=64, help="CPU-oracle sample cells per config (0: skip)")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     hbm = bench.peaks()[0] if hasattr(bench, "peaks") else 6540.8
@@ -33,6 +34,15 @@ def main():
     G.synth_cells(3, offs, 1, 0, *axes)
     ctx = api.context()
     rows = []
+    threads = os.cpu_count() or 1
+    if a.cpu_cells:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+        stride = max(1, a.cells // a.cpu_cells)
+        sel = np.arange(0, a.cells, stride)[:a.cpu_cells]
+        idx = np.concatenate([np.arange(c * a.per, (c + 1) * a.per) for c in sel])
+        hv = np.asfortranarray(np.stack([ax.cpu().numpy()[idx] for ax in axes], axis=1))
+        hoffs = np.arange(len(sel) + 1, dtype=np.int64) * a.per
     for nb in (16, 24, 32, 48, 64):
         b = G.CellBatch(axes, offs, nb, [-6] * 3, [6] * 3)
         for K in (1, 2, 4, 8):
@@ -60,15 +70,25 @@ def main():
                    "em_frac": flops / em_ms / 1e9 / fp64_peak, "mean_iterations": float(r.iterations.mean()),
                    "mean_nnz": float(nnz.mean()), "particles_per_s": a.cells * a.per / (total_ms * 1e-3),
                    "fits_per_s": a.cells / (total_ms * 1e-3)}
+            if a.cpu_cells:  # the CPU oracle (reference algorithm, oracle/) on a cell sample
+                import time
+                t0 = time.perf_counter()
+                O.compress_cells(O.CellsHost(hv, hoffs, nb, [-6] * 3, [6] * 3), cfg, threads=threads)
+                dt = time.perf_counter() - t0
+                row["cpu_particles_per_s"] = len(sel) * a.per / dt
+                row["cpu_fits_per_s"] = len(sel) / dt
+                row["gpu_over_cpu"] = row["particles_per_s"] / row["cpu_particles_per_s"]
             rows.append(row)
     print(f"one B200, {a.cells} cells x {a.per} particles (3V), FP64 peak {fp64_peak:.1f} TFLOP/s, "
-          f"HBM {hbm:.0f} GB/s\n")
-    print("| bins | K | hist kernel | hist ms | hist % HBM | EM ms | EM TFLOP/s | EM % FP64 | mean its | particles/s | fits/s |")
-    print("|---|---|---|---|---|---|---|---|---|---|---|")
+          f"HBM {hbm:.0f} GB/s; CPU = oracle/ (reference algorithm restated) on {a.cpu_cells} sampled cells, "
+          f"{threads} host threads\n")
+    print("| bins | K | hist kernel | hist ms | hist % HBM | EM ms | EM TFLOP/s | EM % FP64 | mean its | particles/s | fits/s | CPU particles/s | GPU/CPU |")
+    print("|---|---|---|---|---|---|---|---|---|---|---|---|---|")
     for r in rows:
+        cpu = f"{r['cpu_particles_per_s']:.3g} | {r['gpu_over_cpu']:.0f}" if "cpu_particles_per_s" in r else "- | -"
         print(f"| {r['n_bins']}³ | {r['K']} | {r['hist_kernel']} | {r['hist_ms']:.2f} | {100 * r['hist_frac']:.1f} | "
               f"{r['em_ms']:.1f} | {r['em_TFLOPs']:.2f} | {100 * r['em_frac']:.1f} | {r['mean_iterations']:.1f} | "
-              f"{r['particles_per_s']:.3g} | {r['fits_per_s']:.3g} |")
+              f"{r['particles_per_s']:.3g} | {r['fits_per_s']:.3g} | {cpu} |")
     if a.json:
         with open(a.json, "w") as f:
             json.dump(rows, f, indent=1)
