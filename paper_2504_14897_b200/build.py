@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libvdfcg.so")
-SOURCES = ["ctx.cu", "hist.cu", "index.cu", "em.cu", "em_d2.cu", "em_d3.cu", "em_entry.cu", "pack.cu", "synth.cu", "metrics.cu",
+SOURCES = ["ctx.cu", "hist.cu", "index.cu", "em.cu", "em_d2.cu", "em_d3.cu", "em_entry.cu", "pack.cu", "synth.cu", "mtjump.cu", "metrics.cu",
            "stream.cu", "multi.cu", "api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",

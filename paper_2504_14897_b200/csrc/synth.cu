@@ -171,10 +171,17 @@ __global__ void generate_kernel(int d, int m, int64_t n, const uint64_t* __restr
   }
 }
 
+void launch_mt_serial(vdfcg_ctx* ctx, uint64_t seed, int64_t count, uint64_t* out) {
+  VDFCG_LAUNCH(ctx, "mt19937_64_stream", mt_stream_kernel<<<1, kMtM, 0, ctx->stream>>>(seed, count, out));
+}
+
+bool launch_mt_stream_jump(vdfcg_ctx* ctx, uint64_t seed, int64_t count, uint64_t* out);  // mtjump.cu
+
 void launch_generate(vdfcg_ctx* ctx, int d, int m, int64_t n, uint64_t seed, uint64_t* uniforms,
                      int64_t n_uniforms, const double* params, double* vel) {
-  VDFCG_LAUNCH(ctx, "mt19937_64_stream",
-               mt_stream_kernel<<<1, kMtM, 0, ctx->stream>>>(seed, n_uniforms, uniforms));
+  // long streams: base window + one CTA per 2^18-word chunk (GF(2) jump-ahead, mtjump.cu);
+  // short ones: the single-CTA twist
+  if (!launch_mt_stream_jump(ctx, seed, n_uniforms, uniforms)) launch_mt_serial(ctx, seed, n_uniforms, uniforms);
   const int grid = static_cast<int>(std::max<int64_t>(
       1, std::min<int64_t>((n + 255) / 256, static_cast<int64_t>(ctx->sm_count) * 16)));
   VDFCG_LAUNCH(ctx, "generate",

@@ -76,3 +76,31 @@ def test_register_pair_twist_matches_mt19937_64():
         A, B = nA, nB
         out += [_temper(x) for x in A + B]
     np.testing.assert_array_equal(np.array(out), O.uniforms(seed, 3 * 312))
+
+
+@pytest.mark.parametrize("offset", [1, 2, 311, 312, 313, 19937, 262145, 1_000_003, 12_000_000])
+def test_mt19937_64_jump_window_matches_sequential_stream(offset):
+    """mtjump.cu: the 312 raw words at stream offset J >= 1 as a GF(2) correlation of the first
+    19937 + 312 words with x^(J-1) mod phi (phi from Berlekamp-Massey) equal the sequential
+    mt19937_64 stream — checked through the tempered top-53-bit uniforms the reference draws
+    (rng.hpp:22) against the oracle's std::mt19937_64. Host-only (no device)."""
+    import ctypes as C
+
+    import numpy as np
+
+    import oracle as O
+    from paper_2504_14897_b200 import api
+    lib = api.lib()
+    fn = lib.vdfcg_debug_mt_window
+    fn.argtypes = [C.c_uint64, C.c_uint64, C.c_void_p]
+    seed = 0x1234567 + offset
+    raw = np.zeros(312, np.uint64)
+    assert fn(seed, offset, raw.ctypes.data) == 0
+    y = raw.copy()
+    y ^= (y >> np.uint64(29)) & np.uint64(0x5555555555555555)
+    y ^= (y << np.uint64(17)) & np.uint64(0x71D67FFFEDA60000)
+    y ^= (y << np.uint64(37)) & np.uint64(0xFFF7EEE000000000)
+    y ^= y >> np.uint64(43)
+    got = (y >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    ref = O.uniforms(seed, offset + 312)[offset:]
+    assert np.array_equal(got, ref)

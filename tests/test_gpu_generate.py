@@ -30,11 +30,20 @@ def _check(fr, mu, cv, n, seed):
     return g
 
 
+def test_generate_jump_ahead_chunk_boundaries():
+    """Streams of >= 2^20 raw words run one CTA per 2^18-word chunk from GF(2) jump-ahead
+    windows (mtjump.cu): particles whose uniforms straddle chunk boundaries must still match
+    the sequential stream (2V: 3 raw words per particle, boundaries at 1 + c 2^18)."""
+    g = _check([0.5, 0.5], [[0, 0], [1, -1]], [np.eye(2), np.array([[0.5, 0.2], [0.2, 0.3]])],
+               600_000, 123)
+    assert g.velocities.shape == (600_000, 2)
+
+
 def test_generate_cfg1_2v():
     _check([0.8, 0.2], [[0, 0], [3, 0]], [np.eye(2), 0.25 * np.eye(2)], 1_000_000, 11)
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 311, 312, 313, 100_001])
+@pytest.mark.parametrize("n", [1, 2, 3, 311, 312, 313, 100_001, 3_000_001])
 def test_generate_3v_full_covariance_odd_spares(n):
     # d = 3: the third normal of an even particle opens a pair whose spare is the first
     # normal of the next particle; n around the 312-word twist block and odd n.
