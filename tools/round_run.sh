@@ -14,11 +14,14 @@ CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu"
 timeout 600 $CMD > $OUT/plain.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1
 # full capture of the two top kernels on the SAME bench command (first launch of each)
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"em_kernel|cells_bitmap|cells_sort|cells_dense" -c 2 -o $OUT/prof_round $CMD > $OUT/ncu_full.log 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"em_kernel|cells_bitmap|cells_sort|cells_dense|ix_downsweep" -c 4 -o $OUT/prof_round $CMD > $OUT/ncu_full.log 2>&1
 if [ "${ROUND_EXTRA:-1}" = "1" ]; then
   timeout 300 python tools/prof_fit.py > $OUT/fit_latency.txt 2>&1
   timeout 300 python tools/prof_metrics.py > $OUT/metrics_time.txt 2>&1
   timeout 300 python tools/prof_metrics.py --d 2 --bins 64 --cells 65536 --per 5000 >> $OUT/metrics_time.txt 2>&1
   timeout 1200 python tools/sweep.py --json $OUT/sweep.json > $OUT/sweep.md 2>&1
+  timeout 300 python tools/prof_generate.py > $OUT/gen_time.txt 2>&1
+  timeout 300 python tools/prof_indexed.py > $OUT/indexed_time.txt 2>&1
+  timeout 300 python tools/prof_indexed.py --sorted >> $OUT/indexed_time.txt 2>&1
 fi
 echo done
