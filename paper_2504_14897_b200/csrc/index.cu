@@ -143,7 +143,10 @@ VDFCG_DEV void tile_rank(const uint32_t (&cell)[kIxIpt], int shift, uint32_t (&r
   constexpr int DIG = 1 << RB;
   constexpr int DPT = DIG >= kIxBlock ? DIG / kIxBlock : 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int t = threadIdx.x; t < kIxWarps * DIG; t += kIxBlock) wcnt[t] = 0u;
+  {
+    uint4* w4 = reinterpret_cast<uint4*>(wcnt);
+    for (int t = threadIdx.x; t < kIxWarps * DIG / 4; t += kIxBlock) w4[t] = make_uint4(0u, 0u, 0u, 0u);
+  }
   __syncthreads();
   uint32_t* my = wcnt + warp * DIG;
   const uint32_t lt = lanemask_lt();
@@ -195,22 +198,15 @@ VDFCG_DEV void tile_rank(const uint32_t (&cell)[kIxIpt], int shift, uint32_t (&r
   __syncthreads();
   const uint32_t base = s_tot[warp] + incl - tot;  // exclusive prefix of this thread's digits
   if (owns) {
-    uint32_t run = base;
 #pragma unroll
     for (int k = 0; k < DPT; ++k) {
       const int d = threadIdx.x * DPT + k;
-      tstart[d] = run;
-      uint32_t last = 0;
+      // wcnt holds the exclusive prefix within this thread's digits: rebase it; warp 0's
+      // entry is the digit's first tile position
+      tstart[d] = base + wcnt[d];
 #pragma unroll
-      for (int w = 0; w < kIxWarps; ++w) {
-        // wcnt holds the exclusive prefix within this thread's digits: rebase it
-        const uint32_t v = wcnt[w * DIG + d];
-        wcnt[w * DIG + d] = base + v;
-        last = v;
-      }
-      (void)last;
+      for (int w = 0; w < kIxWarps; ++w) wcnt[w * DIG + d] += base;
     }
-    (void)run;
   }
   if (threadIdx.x == 0) tstart[DIG] = kIxTile;
   __syncthreads();
