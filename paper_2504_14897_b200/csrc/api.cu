@@ -1024,7 +1024,10 @@ class PageableStager {
       const int slot = static_cast<int>(i % slots);
       // the slot's previous piece must have been issued (its event recorded) and copied
       if (i >= size_t(slots)) {
-        while (!issued_[i - slots].load(std::memory_order_acquire)) std::this_thread::yield();
+        while (!issued_[i - slots].load(std::memory_order_acquire)) {
+          if (failed_) return;
+          std::this_thread::yield();
+        }
         if (cudaEventSynchronize(ctx_->ring_ev[slot]) != cudaSuccess) return fail("staging H2D failed");
       }
       char* buf = static_cast<char*>(ctx_->ring) + size_t(slot) * ctx_->ring_slot;
