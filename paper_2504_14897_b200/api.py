@@ -269,5 +269,6 @@ def validate_fit_config(config: FitConfig, d: int) -> None:
 from .codec import (DecodedModel, decode_histogram, decode_model,  # noqa: E402,F401
                     encode_histogram, histogram_sidecar, model_from_json, model_to_json)
 from .stream import RecordStream, read_index, read_record  # noqa: E402,F401
-from .cells import (CellBatch, CellMetrics, bin_cells, cell_metrics,  # noqa: E402,F401
-                    compress_cells, fit_cells, pack_cells, synth_cells)
+from .cells import (CellBatch, CellMetrics, MultiDevice, ParticleBatch, bin_cells,  # noqa: E402,F401
+                    bin_cells_indexed, cell_metrics, compress_cells, compress_cells_indexed,
+                    fit_cells, pack_cells, partition_cells, synth_cells)
