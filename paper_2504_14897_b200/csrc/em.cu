@@ -319,10 +319,19 @@ void launch_em_cells(vdfcg_ctx* ctx, int d, const KeyCells& kc, const EmConfig& 
     cl = std::min(cl, (2 * ctx->sm_count + fits - 1) / fits);
     if (cl <= 2) cl = 1;  // measured: 2-CTA clusters lose to one CTA (cfg3 2.55 vs 1.88 ms)
   }
+  // VDFCG_EM_SHAPE="G,cl": force warps per CTA and CTAs per cell (measurements only)
+  int Gs = G;
+  if (const char* e = getenv("VDFCG_EM_SHAPE")) {
+    int g2 = 0, c2 = 0;
+    if (sscanf(e, "%d,%d", &g2, &c2) == 2 && g2 >= 1 && g2 <= 8 && c2 >= 1 && c2 <= 16) {
+      Gs = g2;
+      cl = c2;
+    }
+  }
   k2.cluster = cl;
   CoordArgs ca{};
-  if (d == 2) launch_em_dim2(ctx, true, K, k2, ca, cfg, out, kc.n_cells, G, kc.n_bins);
-  else launch_em_dim3(ctx, true, K, k2, ca, cfg, out, kc.n_cells, G, kc.n_bins);
+  if (d == 2) launch_em_dim2(ctx, true, K, k2, ca, cfg, out, kc.n_cells, Gs, kc.n_bins);
+  else launch_em_dim3(ctx, true, K, k2, ca, cfg, out, kc.n_cells, Gs, kc.n_bins);
 }
 
 void launch_fit_prologue(vdfcg_ctx* ctx, int d, const double* pts, const double* w, int64_t n,
