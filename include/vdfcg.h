@@ -401,6 +401,13 @@ int vdfcg_compress_cells_indexed(vdfcg_ctx* ctx, const vdfcg_particles* particle
                                  vdfcg_cell_bins* bins, vdfcg_cell_results* out,
                                  const vdfcg_model_meta* meta, uint8_t* records,
                                  int64_t capacity, int64_t* record_offsets);
+/* ... with the per-cell warm start of vdfcg_fit_cells_warm (the in-situ time series,
+ * pipeline.cpp:482-564): cell id c restarts from warm's model of cell c. */
+int vdfcg_compress_cells_indexed_warm(vdfcg_ctx* ctx, const vdfcg_particles* particles,
+                                      const vdfcg_fit_config* cfg, const vdfcg_cell_results* warm,
+                                      int64_t* cell_offsets, vdfcg_cell_bins* bins,
+                                      vdfcg_cell_results* out, const vdfcg_model_meta* meta,
+                                      uint8_t* records, int64_t capacity, int64_t* record_offsets);
 
 /* ---- Several devices from one host process (run_pipeline's fan-out over
  * parts and final gather, pipeline.cpp:340-353). Cells are independent, so a batch is split

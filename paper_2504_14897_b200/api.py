@@ -61,6 +61,7 @@ def _bind(lib) -> None:
         "vdfcg_compress_cells_warm": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, i64, vp]),
         "vdfcg_bin_cells_indexed": (C.c_int, [vp, vp, vp, vp]),
         "vdfcg_compress_cells_indexed": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, i64, vp]),
+        "vdfcg_compress_cells_indexed_warm": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, vp]),
         "vdfcg_partition_cells": (C.c_int, [vp, i32, i32, vp]),
         "vdfcg_multi_create": (C.c_int, [vp, i32, C.POINTER(vp)]),
         "vdfcg_multi_destroy": (C.c_int, [vp]),

@@ -324,14 +324,15 @@ def bin_cells_indexed(batch: ParticleBatch, out: Optional[CellBins] = None):
 
 def compress_cells_indexed(batch: ParticleBatch, config: FitConfig,
                            meta: Optional[ModelMeta] = None, trace: bool = False,
-                           keep_bins: bool = True):
+                           keep_bins: bool = True, warm: Optional[CellResults] = None):
     """group by cell -> bin -> fit (-> pack) on the device. Returns
-    (cell_offsets, bins, results, records, record_offsets); cell c is cell id c."""
+    (cell_offsets, bins, results, records, record_offsets); cell c is cell id c.
+    `warm`: the previous cycle's results — cell c restarts from its own model."""
     api = _api()
     d = batch.d
     wm = _abi.ModelBuffers.from_model(config.warm_start) if config.warm_start is not None else None
     cfg = _abi.fit_config_struct(config, d, wm)
-    k = max(config.initial_components, wm.k if wm else 0)
+    k = max(config.initial_components, wm.k if wm else 0, warm.k if warm is not None else 0)
     like = batch.axes[0]
     offs = _empty(like, (batch.n_cells + 1,), "i64")
     bins = None
@@ -351,8 +352,10 @@ def compress_cells_indexed(batch: ParticleBatch, config: FitConfig,
         cap = batch.n_cells * per
         rec = _empty(like, (max(cap, 1),), "u8")
         roffs = _empty(like, (batch.n_cells + 1,), "i64")
-    _check(api.lib().vdfcg_compress_cells_indexed(
-        _ctx(like, results.weights).handle, C.byref(batch.struct), C.byref(cfg), _ptr(offs),
+    ws = warm.struct() if warm is not None else None
+    _check(api.lib().vdfcg_compress_cells_indexed_warm(
+        _ctx(like, results.weights).handle, C.byref(batch.struct), C.byref(cfg),
+        C.byref(ws) if ws is not None else None, _ptr(offs),
         C.byref(bs) if bs is not None else None, C.byref(rs),
         C.byref(ms) if ms is not None else None, _ptr(rec), cap, _ptr(roffs)))
     if rec is not None:

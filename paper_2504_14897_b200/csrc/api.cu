@@ -1359,6 +1359,15 @@ int vdfcg_compress_cells_indexed(vdfcg_ctx* ctx, const vdfcg_particles* particle
                                  vdfcg_cell_bins* bins, vdfcg_cell_results* out,
                                  const vdfcg_model_meta* meta, uint8_t* records, int64_t capacity,
                                  int64_t* record_offsets) {
+  return vdfcg_compress_cells_indexed_warm(ctx, particles, cfg, nullptr, cell_offsets, bins, out, meta,
+                                           records, capacity, record_offsets);
+}
+
+int vdfcg_compress_cells_indexed_warm(vdfcg_ctx* ctx, const vdfcg_particles* particles,
+                                      const vdfcg_fit_config* cfg, const vdfcg_cell_results* warm,
+                                      int64_t* cell_offsets, vdfcg_cell_bins* bins,
+                                      vdfcg_cell_results* out, const vdfcg_model_meta* meta,
+                                      uint8_t* records, int64_t capacity, int64_t* record_offsets) {
   return guard_impl([&] {
     begin(ctx);
     IndexedDev in = stage_particles(ctx, particles);
@@ -1373,7 +1382,7 @@ int vdfcg_compress_cells_indexed(vdfcg_ctx* ctx, const vdfcg_particles* particle
     CellBinsDev b = bins_dev(ctx, c, bins, fin);
     EmOut o = results_dev(ctx, c.n_cells, c.d, out, fin);
     launch_bin_cells(ctx, c, b);
-    fit_cells_dev(ctx, c, b, cfg, o);
+    fit_cells_dev(ctx, c, b, cfg, o, warm);
     pack_into(ctx, c, o, meta, records, capacity, record_offsets, fin);
     finish(ctx, offs);
     for (auto& f : fin) f();

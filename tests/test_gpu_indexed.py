@@ -135,3 +135,24 @@ def test_compress_indexed_equals_grouped_path(weighted):
         assert np.array_equal(getattr(r1, f), getattr(r2, f)), f
     assert np.array_equal(ro1, ro2)
     assert bytes(rec1) == bytes(rec2)
+
+
+def test_compress_indexed_warm_start_equals_grouped_warm():
+    """Time series with unsorted particles: cycle 2 restarts every cell from its cycle-1
+    model (pipeline.cpp:482-564) — identical to the grouped path's warm start."""
+    n_cells, n = 300, 300 * 1200
+    v, cell, _ = _case(n, n_cells, 3, seed=21)
+    lo, hi = [-5.0] * 3, [5.0] * 3
+    order = np.argsort(cell, kind="stable")
+    offs_ref = np.zeros(n_cells + 1, np.int64)
+    np.cumsum(np.bincount(cell, minlength=n_cells), out=offs_ref[1:])
+    cfg = FitConfig(initial_components=3, max_em_iterations=50, seed=4)
+    pb = G.ParticleBatch(v, cell, n_cells, 32, lo, hi)
+    _, _, r1, _, _ = G.compress_cells_indexed(pb, cfg)
+    v2 = v + 0.05
+    _, _, r2, _, _ = G.compress_cells_indexed(G.ParticleBatch(v2, cell, n_cells, 32, lo, hi), cfg, warm=r1)
+    gb = G.CellBatch(np.ascontiguousarray(v2[order]), offs_ref, 32, lo, hi)
+    _, g2, _, _ = G.compress_cells(gb, cfg, warm=r1)
+    for f in ("status", "components", "iterations", "weights", "means", "covariances", "final_loglik"):
+        assert np.array_equal(getattr(r2, f), getattr(g2, f)), f
+    assert np.mean(r2.iterations) < np.mean(r1.iterations) + 1  # warm restarts are no slower
