@@ -408,7 +408,7 @@ void log_component_densities(Model& m, const Points& p, std::vector<double>& log
                              std::vector<int>* unrepairable) {
   const int M = static_cast<int>(m.c.size());
   const int d = m.d;
-  logp.assign(static_cast<size_t>(M) * p.n, 0.0);
+  logp.resize(static_cast<size_t>(M) * p.n);  // every entry is written below
   const double log2pi = std::log(2.0 * M_PI);
   for (int i = 0; i < M; ++i) {
     Comp& c = m.c[i];
@@ -433,16 +433,39 @@ void log_component_densities(Model& m, const Points& p, std::vector<double>& log
     double logdet_half = 0.0;
     for (int k = 0; k < d; ++k) logdet_half += std::log(L[k][k]);
     const double cst = d * log2pi + 2.0 * logdet_half;
-    for (int64_t n = 0; n < p.n; ++n) {
-      double y[3];
-      for (int a = 0; a < d; ++a) {  // forward substitution L y = (x - mu)
-        double v = p.at(n, a) - c.mu[a];
-        for (int b = 0; b < a; ++b) v -= L[a][b] * y[b];
-        y[a] = v / L[a][a];
+    // forward substitution L y = (x - mu), per axis in Eigen's order; d is unrolled
+    // (same operations, same order) so the port is a fair CPU baseline
+    const double* x0 = p.x.data();
+    const double* x1 = x0 + p.n;
+    const double* x2 = x1 + p.n;
+    double* out = logp.data() + i;
+    if (d == 2) {
+      for (int64_t n = 0; n < p.n; ++n) {
+        const double y0 = (x0[n] - c.mu[0]) / L[0][0];
+        const double y1 = ((x1[n] - c.mu[1]) - L[1][0] * y0) / L[1][1];
+        const double q = y0 * y0 + y1 * y1;
+        out[n * M] = -0.5 * (q + cst) + log_alpha;
       }
-      double q = 0.0;
-      for (int a = 0; a < d; ++a) q += y[a] * y[a];
-      logp[i + n * M] = -0.5 * (q + cst) + log_alpha;
+    } else if (d == 3) {
+      for (int64_t n = 0; n < p.n; ++n) {
+        const double y0 = (x0[n] - c.mu[0]) / L[0][0];
+        const double y1 = ((x1[n] - c.mu[1]) - L[1][0] * y0) / L[1][1];
+        const double y2 = (((x2[n] - c.mu[2]) - L[2][0] * y0) - L[2][1] * y1) / L[2][2];
+        const double q = (y0 * y0 + y1 * y1) + y2 * y2;
+        out[n * M] = -0.5 * (q + cst) + log_alpha;
+      }
+    } else {
+      for (int64_t n = 0; n < p.n; ++n) {
+        double y[3];
+        for (int a = 0; a < d; ++a) {
+          double v = p.at(n, a) - c.mu[a];
+          for (int b = 0; b < a; ++b) v -= L[a][b] * y[b];
+          y[a] = v / L[a][a];
+        }
+        double q = 0.0;
+        for (int a = 0; a < d; ++a) q += y[a] * y[a];
+        out[n * M] = -0.5 * (q + cst) + log_alpha;
+      }
     }
   }
 }
@@ -465,9 +488,10 @@ double e_step_impl(Model& m, const Points& p, std::vector<double>& resp,
   log_component_densities(m, p, logp, &unrepairable);
   if (static_cast<int>(unrepairable.size()) == M)
     throw std::runtime_error("all mixture components are degenerate");
-  resp.assign(static_cast<size_t>(M) * p.n, 0.0);
+  resp.resize(static_cast<size_t>(M) * p.n);  // every entry is written below
   Kahan ll;
-  std::vector<double> u(M);
+  thread_local std::vector<double> u;
+  u.resize(M);
   for (int64_t n = 0; n < p.n; ++n) {
     const double* col = &logp[n * M];
     double mx = col[0];
@@ -490,11 +514,41 @@ Model m_step_impl(const Points& p, double total, const std::vector<double>& resp
   const int M = static_cast<int>(prev.c.size());
   const int d = p.d;
   if (!(total > 0.0)) throw std::runtime_error("m_step: zero total weight");
+  // one pass per component for the mass and the first moments (each sum keeps the
+  // sequential order over n; the mass check below still precedes any use)
   std::vector<double> mass(M, 0.0);
+  thread_local std::vector<double> wi, sms;
+  wi.resize(static_cast<size_t>(M) * p.n);
+  sms.assign(static_cast<size_t>(M) * 3, 0.0);
   for (int i = 0; i < M; ++i) {
-    double s = 0.0;
-    for (int64_t n = 0; n < p.n; ++n) s += resp[i + n * M] * p.w[n];
+    double* wr = &wi[static_cast<size_t>(i) * p.n];
+    double s = 0.0, s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    const double* x0 = p.x.data();
+    const double* x1 = x0 + p.n;
+    const double* x2 = x1 + p.n;
+    const double* r = resp.data() + i;
+    if (d == 3) {
+      for (int64_t n = 0; n < p.n; ++n) {
+        const double v = r[n * M] * p.w[n];
+        wr[n] = v;
+        s += v;
+        s0 += x0[n] * v;
+        s1 += x1[n] * v;
+        s2 += x2[n] * v;
+      }
+    } else {
+      for (int64_t n = 0; n < p.n; ++n) {
+        const double v = r[n * M] * p.w[n];
+        wr[n] = v;
+        s += v;
+        s0 += x0[n] * v;
+        if (d > 1) s1 += x1[n] * v;
+      }
+    }
     mass[i] = s;
+    sms[i * 3 + 0] = s0;
+    sms[i * 3 + 1] = s1;
+    sms[i * 3 + 2] = s2;
   }
   for (int i = 0; i < M; ++i)
     if (!std::isfinite(mass[i]) || mass[i] < 0.0)
@@ -506,8 +560,6 @@ Model m_step_impl(const Points& p, double total, const std::vector<double>& resp
   std::memcpy(out.scale, prev.scale, sizeof(out.scale));
   std::memcpy(out.offset, prev.offset, sizeof(out.offset));
   out.c.resize(M);
-  thread_local std::vector<double> wi;
-  wi.resize(p.n);
   for (int i = 0; i < M; ++i) {
     Comp& c = out.c[i];
     c.w = mass[i] / total;
@@ -516,19 +568,36 @@ Model m_step_impl(const Points& p, double total, const std::vector<double>& resp
       c.cov = prev.c[i].cov;
       continue;
     }
-    for (int64_t n = 0; n < p.n; ++n) wi[n] = resp[i + n * M] * p.w[n];
-    // one pass per moment order; every entry keeps the sequential order over n
-    double sm[3] = {0.0, 0.0, 0.0};
-    for (int64_t n = 0; n < p.n; ++n)
-      for (int a = 0; a < d; ++a) sm[a] += p.at(n, a) * wi[n];
+    const double* wr = &wi[static_cast<size_t>(i) * p.n];
+    const double* sm = &sms[i * 3];
     for (int a = 0; a < d; ++a) c.mu[a] = sm[a] / mass[i];
     Mat3 sigma{};
     double ss[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-    for (int64_t n = 0; n < p.n; ++n) {
-      double cen[3];
-      for (int a = 0; a < d; ++a) cen[a] = p.at(n, a) - c.mu[a];
-      for (int a = 0; a < d; ++a)
-        for (int b = a; b < d; ++b) ss[a][b] += (cen[a] * wi[n]) * cen[b];
+    if (d == 3) {
+      const double* x0 = p.x.data();
+      const double* x1 = x0 + p.n;
+      const double* x2 = x1 + p.n;
+      const double m0 = c.mu[0], m1 = c.mu[1], m2 = c.mu[2];
+      double s00 = 0.0, s01 = 0.0, s02 = 0.0, s11 = 0.0, s12 = 0.0, s22 = 0.0;
+      for (int64_t n = 0; n < p.n; ++n) {
+        const double c0 = x0[n] - m0, c1 = x1[n] - m1, c2 = x2[n] - m2;
+        const double a0 = c0 * wr[n], a1 = c1 * wr[n], a2 = c2 * wr[n];
+        s00 += a0 * c0;
+        s01 += a0 * c1;
+        s02 += a0 * c2;
+        s11 += a1 * c1;
+        s12 += a1 * c2;
+        s22 += a2 * c2;
+      }
+      ss[0][0] = s00; ss[0][1] = s01; ss[0][2] = s02;
+      ss[1][1] = s11; ss[1][2] = s12; ss[2][2] = s22;
+    } else {
+      for (int64_t n = 0; n < p.n; ++n) {
+        double cen[3] = {0.0, 0.0, 0.0};
+        for (int a = 0; a < d; ++a) cen[a] = p.at(n, a) - c.mu[a];
+        for (int a = 0; a < d; ++a)
+          for (int b = a; b < d; ++b) ss[a][b] += (cen[a] * wr[n]) * cen[b];
+      }
     }
     for (int a = 0; a < d; ++a)
       for (int b = a; b < d; ++b) sigma[a][b] = ss[a][b] / mass[i];
