@@ -535,7 +535,8 @@ __global__ void __launch_bounds__(512) cells_compact_kernel(
 // K3: per-cell composite-key sort. key = (bin << IDXB) | local index; OOR bin = SENT.
 // Unit weights sort the bin key alone (counts = run lengths; order within a run is
 // irrelevant); fractional weights sort (bin, particle) so each run is summed in particle
-// order. 6-bit digits: 3 passes for 48^3 / 64^3 bins on the unit-weight path.
+// order. CUB's 4-bit digits: 5- and 6-bit digits measured slower at 64^3 (2.06 / 3.09
+// vs 1.97 ms per 65536 cells; the wider rank counters cost occupancy).
 template <int D, int BLOCK, int IPT, bool W>
 __global__ void __launch_bounds__(BLOCK) cells_sort_kernel(
     VelPtrs vp, const double* __restrict__ w, const int64_t* __restrict__ offsets, int n_cells,
@@ -876,10 +877,13 @@ struct StageShift {
   int sh[3];
 };
 
-template <int D, int BLOCK, int kTmaWpt, bool GEN, int MINB>  // kTmaWpt >= bitmap words per
-// thread; GEN: some array base is not 16-byte aligned (per-array skew), else the aligned
-// fast form; MINB: CTAs per SM the shared memory allows (3 caps registers at 40 for 512
-// threads: small bitmaps run three CTAs, larger ones two with more registers)
+template <int D, int BLOCK, int kTmaWpt, bool GEN, int MINB, bool PK = false>  // kTmaWpt >=
+// bitmap words per thread; GEN: some array base is not 16-byte aligned (per-array skew),
+// else the aligned fast form; MINB: CTAs per SM the shared memory allows (3 caps registers
+// at 40 for 512 threads: small bitmaps run three CTAs, larger ones two with more
+// registers); PK: per-rank counts packed as u16 pairs (a staged cell has < 2^16
+// particles) — only where the 2 bytes per rank saved make room for a third CTA (32^3:
+// 0.567 -> 0.628 of HBM); elsewhere the shift/mask costs ~2%
 __global__ void __launch_bounds__(BLOCK) __maxnreg__(MINB == 3 ? 40 : 48) cells_bitmap_tma_kernel(
     VelPtrs vp, const int64_t* __restrict__ offsets, int n_cells, CellGeom g, int words, int ccap,
     int capp, StageShift ss_, int32_t* nnz, uint32_t* __restrict__ keys_out,
@@ -893,13 +897,15 @@ __global__ void __launch_bounds__(BLOCK) __maxnreg__(MINB == 3 ? 40 : 48) cells_
   unsigned char* pbuf = smem_raw;                                        // [arrays][capp]
   unsigned* bitmap = reinterpret_cast<unsigned*>(pbuf + size_t(S::kArrays) * capp * S::kElem);
   unsigned* wpre = bitmap + words;                                       // [words]
-  unsigned* cnt = wpre + words;                                          // [ccap]
-  unsigned* kbuf = cnt + ccap;                                           // [capp]
+  const int cw = PK ? (ccap + 1) >> 1 : ccap;
+  unsigned* cnt2 = wpre + words;                                         // [cw]
+  unsigned* kbuf = cnt2 + cw;                                            // [capp]
   unsigned* keyr = kbuf + capp;                                          // [ccap] key of rank r
+  unsigned short* cnt16 = reinterpret_cast<unsigned short*>(cnt2);
   const int wpt = (words + BLOCK - 1) / BLOCK;
   const int64_t lim = offsets[n_cells];
   for (int t = threadIdx.x; t < words; t += BLOCK) bitmap[t] = 0u;
-  for (int t = threadIdx.x; t < ccap; t += BLOCK) cnt[t] = 0u;
+  for (int t = threadIdx.x; t < cw; t += BLOCK) cnt2[t] = 0u;
   if (threadIdx.x == 0) {
     s_oor = 0u;
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)) : "memory");
@@ -978,7 +984,8 @@ __global__ void __launch_bounds__(BLOCK) __maxnreg__(MINB == 3 ? 40 : 48) cells_
       if (key != 0xffffffffu) {
         const unsigned wd = key >> 5, bit = key & 31;
         const unsigned r = wpre[wd] + __popc(bitmap[wd] & ((1u << bit) - 1u));
-        atomicAdd(cnt + r, 1u);
+        if constexpr (PK) atomicAdd(cnt2 + (r >> 1), 1u << ((r & 1u) << 4));
+        else atomicAdd(cnt2 + r, 1u);
         keyr[r] = key;  // duplicates store the same value
       }
     }
@@ -986,8 +993,13 @@ __global__ void __launch_bounds__(BLOCK) __maxnreg__(MINB == 3 ? 40 : 48) cells_
     // 4. emit counts, re-zero
     for (unsigned r = threadIdx.x; r < total; r += BLOCK) {  // coalesced keys + counts
       keys_out[b + r] = keyr[r];
-      counts_out[b + r] = static_cast<double>(cnt[r]);
-      cnt[r] = 0u;
+      if constexpr (PK) {
+        counts_out[b + r] = static_cast<double>(cnt16[r]);
+        cnt16[r] = 0;
+      } else {
+        counts_out[b + r] = static_cast<double>(cnt2[r]);
+        cnt2[r] = 0u;
+      }
     }
 #pragma unroll
     for (int k = 0; k < kTmaWpt; ++k)
@@ -1204,8 +1216,9 @@ static void bin_cells_d(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
   // kernel carries each array's offset from a 16-byte boundary (Eigen N x 3 columns).
   using S = Stage<D>;
   const int64_t capp = ((maxc + 2 * (S::kA - 1) + S::kA - 1) / S::kA) * S::kA;
-  const size_t tma_smem = size_t(S::kArrays) * capp * S::kElem + size_t(words) * 8 + size_t(ccap) * 8 +
-                          size_t(capp) * 4;
+  const size_t tma_smem_pk = size_t(S::kArrays) * capp * S::kElem + size_t(words) * 8 +
+                             size_t((ccap + 1) / 2) * 4 + size_t(ccap) * 4 + size_t(capp) * 4;
+  size_t tma_smem = tma_smem_pk + size_t(ccap) * 4 - size_t((ccap + 1) / 2) * 4;
   bool aligned = true;
   StageShift shift{};
   for (int a = 0; a < S::kArrays; ++a) {
@@ -1225,7 +1238,7 @@ static void bin_cells_d(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
     return v == "tma" ? 1 : v == "bitmap" ? 2 : v == "sort" ? 3 : v == "dense" ? 4 : 0;
   }();
   const int tb = tma_env == 2 ? 256 : 512;
-  const bool tma_fits = aligned && tma_env && tma_smem <= 220 * 1024 && words <= 16 * tb;
+  const bool tma_fits = aligned && tma_env && tma_smem <= 220 * 1024 && words <= 16 * tb && maxc < 65536;
   // Unit weights, measured on 65536 cells (tools: exp-style sweeps recorded in DESIGN.md):
   // the TMA bitmap kernel whenever it fits two CTAs per SM (1907 particles/cell,
   // 16^3..48^3: 0.74-1.0 ms, 6x the dense path at 16^3), or one CTA per SM with a bitmap of
@@ -1245,12 +1258,18 @@ static void bin_cells_d(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
     bool gen = false;
     for (int a = 0; a < S::kArrays; ++a) gen = gen || shift.sh[a] != 0;
     const bool three = tma_smem * 3 + 3 * 1024 <= 227 * 1024;
+    const bool three_pk = !three && tma_smem_pk * 3 + 3 * 1024 <= 227 * 1024;
+    if (three_pk) tma_smem = tma_smem_pk;
     using KFn = void (*)(VelPtrs, const int64_t*, int, CellGeom, int, int, int, StageShift, int32_t*,
                          uint32_t*, double*, double*, double*);
     KFn k;
 #define VDFCG_TMA_PICK(B, WPT)                                                                     \
-  k = gen ? (three ? cells_bitmap_tma_kernel<D, B, WPT, true, 3> : cells_bitmap_tma_kernel<D, B, WPT, true, 1>) \
-          : (three ? cells_bitmap_tma_kernel<D, B, WPT, false, 3> : cells_bitmap_tma_kernel<D, B, WPT, false, 1>)
+  k = gen ? (three ? cells_bitmap_tma_kernel<D, B, WPT, true, 3>                                  \
+                   : three_pk ? cells_bitmap_tma_kernel<D, B, WPT, true, 3, true>                  \
+                              : cells_bitmap_tma_kernel<D, B, WPT, true, 1>)                       \
+          : (three ? cells_bitmap_tma_kernel<D, B, WPT, false, 3>                                 \
+                   : three_pk ? cells_bitmap_tma_kernel<D, B, WPT, false, 3, true>                 \
+                              : cells_bitmap_tma_kernel<D, B, WPT, false, 1>)
     if (tb == 512) {
       if (w8) VDFCG_TMA_PICK(512, 8);
       else VDFCG_TMA_PICK(512, 16);

@@ -37,11 +37,14 @@ def test_forced_histogram_path_bit_exact(path, tmp_path):
             assert np.array_equal(g[f"counts{nb}"][b:b + k], ob.counts[b:b + k]), (nb, c)
 
 
-@pytest.mark.parametrize("n_per_cell", [1907, 1906])
-def test_tma_path_accepts_eigen_column_bases(n_per_cell):
+@pytest.mark.parametrize("n_per_cell,nb,eigen", [(1907, 48, True), (1906, 48, True), (1907, 32, True),
+                                                (1907, 32, False), (1200, 32, False)])
+def test_tma_path_accepts_eigen_column_bases(n_per_cell, nb, eigen):
     """An Eigen N x 3 column-major matrix with odd N has its v and w columns 8 bytes off a
     16-byte boundary (ParticleSet::velocities, synthdata.hpp:13-28). The TMA kernel carries
-    the per-axis skew, so such device columns bin bit-exactly (forced TMA path)."""
+    the per-axis skew, so such device columns bin bit-exactly (forced TMA path). 32^3 with
+    ~1.9K particles per cell runs the packed-u16-count form (three CTAs per SM), aligned
+    and skewed."""
     code = f"""
 import sys, numpy as np, torch
 sys.path.insert(0, {ROOT!r})
@@ -53,8 +56,12 @@ v = rng.normal(size=(n, 3)) * 1.5
 offs = np.arange(nc + 1, dtype=np.int64) * {n_per_cell}
 flat = torch.from_numpy(np.asfortranarray(v).reshape(-1, order="F").copy()).cuda()
 cols = [flat[a * n:(a + 1) * n] for a in range(3)]
-assert cols[1].data_ptr() % 16 == 8
-b = G.bin_cells(G.CellBatch(cols, torch.from_numpy(offs).cuda(), 48, [-5] * 3, [5] * 3))
+if {eigen}:
+    assert cols[1].data_ptr() % 16 == 8
+else:
+    cols = [c.clone() for c in cols]
+    assert all(c.data_ptr() % 16 == 0 for c in cols)
+b = G.bin_cells(G.CellBatch(cols, torch.from_numpy(offs).cuda(), {nb}, [-5] * 3, [5] * 3))
 torch.cuda.synchronize()
 np.savez(sys.argv[1], nnz=b.nnz.cpu().numpy(), keys=b.keys.cpu().numpy().view(np.uint32),
          counts=b.counts.cpu().numpy(), v=v, offs=offs)
@@ -66,7 +73,7 @@ np.savez(sys.argv[1], nnz=b.nnz.cpu().numpy(), keys=b.keys.cpu().numpy().view(np
         r = subprocess.run([sys.executable, "-c", code, out], env=env, capture_output=True, text=True, timeout=300)
         assert r.returncode == 0, r.stderr[-2000:]
         g = np.load(out)
-        ob = O.bin_cells(O.CellsHost(g["v"], g["offs"], 48, [-5] * 3, [5] * 3))
+        ob = O.bin_cells(O.CellsHost(g["v"], g["offs"], nb, [-5] * 3, [5] * 3))
         assert np.array_equal(g["nnz"], ob.nnz)
         offs = g["offs"]
         for c in range(len(offs) - 1):
