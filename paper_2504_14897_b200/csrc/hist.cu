@@ -877,13 +877,15 @@ struct StageShift {
   int sh[3];
 };
 
-template <int D, int BLOCK, int kTmaWpt, bool GEN, int MINB, bool PK = false>  // kTmaWpt >=
+template <int D, int BLOCK, int kTmaWpt, bool GEN, int MINB, bool PK = false, int GW = 1>  // kTmaWpt >=
 // bitmap words per thread; GEN: some array base is not 16-byte aligned (per-array skew),
 // else the aligned fast form; MINB: CTAs per SM the shared memory allows (3 caps registers
 // at 40 for 512 threads: small bitmaps run three CTAs, larger ones two with more
 // registers); PK: per-rank counts packed as u16 pairs (a staged cell has < 2^16
 // particles) — only where the 2 bytes per rank saved make room for a third CTA (32^3:
-// 0.567 -> 0.628 of HBM); elsewhere the shift/mask costs ~2%
+// 0.567 -> 0.628 of HBM); elsewhere the shift/mask costs ~2%. GW = 4: one exclusive prefix
+// per 4-word group (a rank adds the popcounts of the group's earlier words, read as one
+// 16-byte load), so a 64^3 bitmap's prefix array shrinks 4x and two CTAs fit per SM
 __global__ void __launch_bounds__(BLOCK) __maxnreg__(MINB == 3 ? 40 : 48) cells_bitmap_tma_kernel(
     VelPtrs vp, const int64_t* __restrict__ offsets, int n_cells, CellGeom g, int words, int ccap,
     int capp, StageShift ss_, int32_t* nnz, uint32_t* __restrict__ keys_out,
@@ -896,13 +898,16 @@ __global__ void __launch_bounds__(BLOCK) __maxnreg__(MINB == 3 ? 40 : 48) cells_
   using S = Stage<D>;
   unsigned char* pbuf = smem_raw;                                        // [arrays][capp]
   unsigned* bitmap = reinterpret_cast<unsigned*>(pbuf + size_t(S::kArrays) * capp * S::kElem);
-  unsigned* wpre = bitmap + words;                                       // [words]
+  unsigned* wpre = bitmap + words;                                       // [words / GW]
   const int cw = PK ? (ccap + 1) >> 1 : ccap;
-  unsigned* cnt2 = wpre + words;                                         // [cw]
+  unsigned* cnt2 = wpre + (words + GW - 1) / GW;                         // [cw]
   unsigned* kbuf = cnt2 + cw;                                            // [capp]
   unsigned* keyr = kbuf + capp;                                          // [ccap] key of rank r
   unsigned short* cnt16 = reinterpret_cast<unsigned short*>(cnt2);
   const int wpt = (words + BLOCK - 1) / BLOCK;
+  // GW = 4: word w lives at w ^ ((w >> 5) & 15) — thread t's k-th prefix word 16t + k then
+  // hits 32 distinct banks across a warp (a plain stride of 16 words is a 16-way conflict)
+  auto swz = [](unsigned w) { return GW == 4 ? (w ^ ((w >> 5) & 15u)) : w; };
   const int64_t lim = offsets[n_cells];
   for (int t = threadIdx.x; t < words; t += BLOCK) bitmap[t] = 0u;
   for (int t = threadIdx.x; t < cw; t += BLOCK) cnt2[t] = 0u;
@@ -948,7 +953,7 @@ __global__ void __launch_bounds__(BLOCK) __maxnreg__(MINB == 3 ? 40 : 48) cells_
         ++oor;
         kbuf[li] = 0xffffffffu;
       } else {
-        atomicOr(bitmap + (key >> 5), 1u << (key & 31));
+        atomicOr(bitmap + swz(static_cast<unsigned>(key >> 5)), 1u << (key & 31));
         kbuf[li] = static_cast<unsigned>(key);
       }
     }
@@ -966,14 +971,18 @@ __global__ void __launch_bounds__(BLOCK) __maxnreg__(MINB == 3 ? 40 : 48) cells_
 #pragma unroll
     for (int k = 0; k < kTmaWpt; ++k) {
       const int wi = threadIdx.x * wpt + k;
-      pc[k] = (k < wpt && wi < words) ? __popc(bitmap[wi]) : 0u;
+      pc[k] = (k < wpt && wi < words) ? __popc(bitmap[swz(wi)]) : 0u;
       local += pc[k];
     }
     unsigned pre, total;
     Scan(ss).ExclusiveSum(local, pre, total);
 #pragma unroll
     for (int k = 0; k < kTmaWpt; ++k) {
-      if (pc[k]) wpre[threadIdx.x * wpt + k] = pre;  // only occupied words are ever read
+      if constexpr (GW == 1) {
+        if (pc[k]) wpre[threadIdx.x * wpt + k] = pre;  // only occupied words are ever read
+      } else {  // wpt is a multiple of GW (host): groups never straddle threads
+        if (k % GW == 0 && k < wpt) wpre[(threadIdx.x * wpt + k) / GW] = pre;
+      }
       pre += pc[k];
     }
     __syncthreads();
@@ -983,7 +992,19 @@ __global__ void __launch_bounds__(BLOCK) __maxnreg__(MINB == 3 ? 40 : 48) cells_
       const unsigned key = kbuf[li];
       if (key != 0xffffffffu) {
         const unsigned wd = key >> 5, bit = key & 31;
-        const unsigned r = wpre[wd] + __popc(bitmap[wd] & ((1u << bit) - 1u));
+        unsigned r;
+        if constexpr (GW == 1) {
+          r = wpre[wd] + __popc(bitmap[wd] & ((1u << bit) - 1u));
+        } else {
+          static_assert(GW == 4, "4-word groups");
+          // the group's 4 words sit in one swizzled 16-byte slot, slot p holding word p ^ s3
+          const unsigned sx = (wd >> 5) & 15u, s3 = sx & 3u;
+          const uint4 q = reinterpret_cast<const uint4*>(bitmap)[((wd & ~3u) ^ (sx & 12u)) >> 2];
+          const unsigned j = wd & 3u, lt = (1u << bit) - 1u;
+          auto msk = [&](unsigned p) { const unsigned l = p ^ s3; return l < j ? ~0u : l == j ? lt : 0u; };
+          r = wpre[wd >> 2] + __popc(q.x & msk(0)) + __popc(q.y & msk(1)) + __popc(q.z & msk(2)) +
+              __popc(q.w & msk(3));
+        }
         if constexpr (PK) atomicAdd(cnt2 + (r >> 1), 1u << ((r & 1u) << 4));
         else atomicAdd(cnt2 + r, 1u);
         keyr[r] = key;  // duplicates store the same value
@@ -1003,7 +1024,7 @@ __global__ void __launch_bounds__(BLOCK) __maxnreg__(MINB == 3 ? 40 : 48) cells_
     }
 #pragma unroll
     for (int k = 0; k < kTmaWpt; ++k)
-      if (pc[k]) bitmap[threadIdx.x * wpt + k] = 0u;
+      if (pc[k]) bitmap[swz(threadIdx.x * wpt + k)] = 0u;
     if (threadIdx.x == 0) {
       const unsigned to = s_oor;
       nnz[c] = static_cast<int32_t>(total);
@@ -1244,11 +1265,16 @@ static void bin_cells_d(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
   // 16^3..48^3: 0.74-1.0 ms, 6x the dense path at 16^3), or one CTA per SM with a bitmap of
   // <= 4096 words (6000/cell, 16^3..32^3: 2.6-3.0 ms vs 6-18 ms dense); else the plain
   // bitmap kernel for bitmaps of <= 4096 words (6000/cell at 48^3: 4.5 ms vs 11.5 sort);
-  // larger bitmaps (64^3) favour the radix sort (1907/cell: 2.0 ms vs 2.4 TMA, 7.6 bitmap).
+  // 64^3 (1907/cell): TMA with 4-word prefix groups at two CTAs/SM 1.44 ms vs 1.97 sort,
+  // 2.4 one-CTA TMA, 7.6 bitmap; larger cells at 64^3 take the radix sort.
   const bool bitmap_fits = words * 8 + ccap * 4 + kcap * 4 <= 160 * 1024;
+  // 4-word prefix groups when only they bring a large bitmap (64^3) to two CTAs per SM
+  const size_t tma_smem_gw = tma_smem - size_t(words) * 4 + size_t((words + 3) / 4) * 4;
+  const bool gw4 = tb == 512 && words > 8 * 512 && ((words + 511) / 512) % 4 == 0 &&
+                   tma_smem > 110 * 1024 && tma_smem_gw <= 110 * 1024;
   int choice = path_env;
   if (choice == 0 && !weighted) {
-    if (tma_fits && tma_smem <= 110 * 1024) choice = 1;
+    if (tma_fits && (tma_smem <= 110 * 1024 || gw4)) choice = 1;
     else if (tma_fits && words <= 4096) choice = 1;
     else if (sparse && bitmap_fits && words <= 4096) choice = 2;
     else if (maxc <= 8192 && sparse) choice = 3;
@@ -1270,7 +1296,11 @@ static void bin_cells_d(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
           : (three ? cells_bitmap_tma_kernel<D, B, WPT, false, 3>                                 \
                    : three_pk ? cells_bitmap_tma_kernel<D, B, WPT, false, 3, true>                 \
                               : cells_bitmap_tma_kernel<D, B, WPT, false, 1>)
-    if (tb == 512) {
+    if (gw4) {
+      tma_smem = tma_smem_gw;
+      k = gen ? cells_bitmap_tma_kernel<D, 512, 16, true, 1, false, 4>
+              : cells_bitmap_tma_kernel<D, 512, 16, false, 1, false, 4>;
+    } else if (tb == 512) {
       if (w8) VDFCG_TMA_PICK(512, 8);
       else VDFCG_TMA_PICK(512, 16);
     } else {
