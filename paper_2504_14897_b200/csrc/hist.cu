@@ -886,7 +886,7 @@ template <int D, int BLOCK, int kTmaWpt, bool GEN, int MINB, bool PK = false, in
 // 0.567 -> 0.628 of HBM); elsewhere the shift/mask costs ~2%. GW = 4: one exclusive prefix
 // per 4-word group (a rank adds the popcounts of the group's earlier words, read as one
 // 16-byte load), so a 64^3 bitmap's prefix array shrinks 4x and two CTAs fit per SM
-__global__ void __launch_bounds__(BLOCK) __maxnreg__(MINB == 3 ? 40 : 48) cells_bitmap_tma_kernel(
+__global__ void __launch_bounds__(BLOCK) __maxnreg__(MINB == 3 ? 40 : GW == 4 ? 64 : 48) cells_bitmap_tma_kernel(
     VelPtrs vp, const int64_t* __restrict__ offsets, int n_cells, CellGeom g, int words, int ccap,
     int capp, StageShift ss_, int32_t* nnz, uint32_t* __restrict__ keys_out,
     double* __restrict__ counts_out, double* oor_out, double* in_range) {
