@@ -15,6 +15,7 @@
 //    weights are summed in particle order, i.e. bit-identical to the reference's
 //    sequential `counts(i,j) += w` (histogram.cpp:70-73).
 // K4 compaction of dense grids (histogram.cpp:86-109 order: i outer, j, k inner).
+#include <cub/block/block_exchange.cuh>
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
@@ -547,7 +548,9 @@ __global__ void __launch_bounds__(BLOCK) cells_sort_kernel(
   using Scan = cub::BlockScan<int, BLOCK>;
   using ReduceD = cub::BlockReduce<double, BLOCK>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  using Exchange = cub::BlockExchange<uint32_t, BLOCK, IPT>;
   auto& sort_ts = *reinterpret_cast<typename Sort::TempStorage*>(smem_raw);
+  auto& exch_ts = *reinterpret_cast<typename Exchange::TempStorage*>(smem_raw);
   uint32_t* sk = reinterpret_cast<uint32_t*>(smem_raw);  // reused after the sort
   uint32_t* pos = sk + CAP;                               // run heads [CAP + 1]
   __shared__ typename Scan::TempStorage ss;
@@ -574,7 +577,15 @@ __global__ void __launch_bounds__(BLOCK) cells_sort_kernel(
     }
     if (W && bad) atomicOr(err, 1);
     __syncthreads();
-    Sort(sort_ts).Sort(k, 0, binbits + (W ? idxbits : 0));
+    if constexpr (W) {
+      // blocked = particle order, so a stable sort on the bin bits alone keeps every
+      // bin's particles in order (5 digit passes at 48^3 instead of 7 over bin + index)
+      Exchange(exch_ts).StripedToBlocked(k);
+      __syncthreads();
+      Sort(sort_ts).Sort(k, idxbits, idxbits + binbits);
+    } else {
+      Sort(sort_ts).Sort(k, 0, binbits);
+    }
     __syncthreads();
     // blocked arrangement: thread t holds sorted positions t*IPT + i
 #pragma unroll
@@ -1110,7 +1121,9 @@ static void launch_sort(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
                         const CellGeom& g, int binbits, int* err) {
   using Sort = cub::BlockRadixSort<uint32_t, BLOCK, IPT>;
   constexpr int CAP = BLOCK * IPT;
-  const size_t smem = std::max(sizeof(typename Sort::TempStorage), size_t(2 * CAP + 2) * 4);
+  const size_t smem = std::max({sizeof(typename Sort::TempStorage),
+                                sizeof(typename cub::BlockExchange<uint32_t, BLOCK, IPT>::TempStorage),
+                                size_t(2 * CAP + 2) * 4});
   auto k = cells_sort_kernel<D, BLOCK, IPT, W>;
   VDFCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int occ = 0;
