@@ -1550,6 +1550,9 @@ int vdfcg_synth_cells(vdfcg_ctx* ctx, int32_t d, int32_t n_cells, const int64_t*
     if (!is_device_pointer(cell_offsets) || !is_device_pointer(u) || !is_device_pointer(v) ||
         (d == 3 && !is_device_pointer(w)))
       throw InvalidArgument("vdfcg_synth_cells takes device pointers");
+    for (const void* q : {static_cast<const void*>(cell_offsets), static_cast<const void*>(u),
+                          static_cast<const void*>(v), static_cast<const void*>(w)})
+      if (q) check_pointer_device(ctx, q);
     if (n_cells > 0) launch_synth(ctx, d, n_cells, cell_offsets, cell_base, seed, species, u, v, w);
   });
 }

@@ -25,6 +25,17 @@ bool is_device_pointer(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+void check_pointer_device(const vdfcg_ctx* ctx, const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  if (a.type == cudaMemoryTypeDevice && a.device != ctx->device)
+    throw InvalidArgument("device pointer on cuda:" + std::to_string(a.device) +
+                          " passed to a context on cuda:" + std::to_string(ctx->device));
+}
+
 void arena_reset(vdfcg_ctx* ctx) {
   for (auto& c : ctx->chunks) c.used = 0;
 }

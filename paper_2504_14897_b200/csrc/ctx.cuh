@@ -31,6 +31,9 @@ void cuda_check(cudaError_t e, const char* what);
 #define VDFCG_CUDA(x) ::vdfcg::cuda_check((x), #x)
 
 bool is_device_pointer(const void* p);
+// Device memory of ANOTHER GPU than the context's cannot be read by its kernels (no peer
+// mapping is set up): such pointers are rejected with the reference's invalid_argument.
+void check_pointer_device(const vdfcg_ctx* ctx, const void* p);
 
 // Runs f, mapping the exceptions above to VDFCG_* codes + the thread-local message.
 int guard_impl(const std::function<void()>& f);
@@ -99,6 +102,7 @@ Staged<T> stage_in(vdfcg_ctx* ctx, const T* p, size_t count) {
   s.count = count;
   if (!p) return s;
   if (is_device_pointer(p)) {
+    check_pointer_device(ctx, p);
     s.dev = const_cast<T*>(p);
     return s;
   }
@@ -116,6 +120,7 @@ Staged<T> stage_out(vdfcg_ctx* ctx, T* p, size_t count) {
   s.count = count;
   if (!p) return s;
   if (is_device_pointer(p)) {
+    check_pointer_device(ctx, p);
     s.dev = p;
     return s;
   }

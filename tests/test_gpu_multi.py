@@ -78,3 +78,22 @@ def test_multi_keeps_bins_and_reports_errors():
     with pytest.raises(ValueError, match="prune_threshold"):
         md.compress_cells(b, bad, None)
     md.close()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two GPUs")
+def test_device_pointer_of_another_gpu_is_rejected():
+    """A context's kernels cannot read another GPU's memory (no peer mapping): the call
+    fails with invalid_argument naming both devices instead of faulting."""
+    import ctypes as C
+    from paper_2504_14897_b200 import api
+    from paper_2504_14897_b200.types import InvalidArgument
+    v = [torch.randn(1000, dtype=torch.float64, device="cuda:1") for _ in range(3)]
+    offs = torch.tensor([0, 1000], dtype=torch.int64, device="cuda:1")
+    b = G.CellBatch(v, offs, 16, [-5.0] * 3, [5.0] * 3)
+    bins = G.CellBins.alloc(b)
+    bs = bins.struct()
+    rc = api.lib().vdfcg_bin_cells(api.context(0).handle, C.byref(b.struct), C.byref(bs))
+    assert rc == 1
+    assert "passed to a context on cuda:0" in api.lib().vdfcg_last_error().decode()
+    with pytest.raises(InvalidArgument):
+        G._check(rc)
