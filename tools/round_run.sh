@@ -10,6 +10,8 @@ nproc > $OUT/nproc.txt
 timeout 600 python __graft_entry__.py > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
 timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err
 timeout 600 python bench.py --impl reference > $OUT/bench_ref.json 2> $OUT/bench_ref.err
+# the FP32 E-step option (not the reference precision; informative only)
+timeout 600 python bench.py --estep-fp32 --no-e2e --no-indexed --no-weighted --no-cpu > $OUT/bench_fp32.json 2> $OUT/bench_fp32.err
 CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu"
 timeout 600 $CMD > $OUT/plain.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1
