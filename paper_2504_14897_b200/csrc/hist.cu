@@ -992,7 +992,7 @@ __global__ void __launch_bounds__(BLOCK) __maxnreg__(MINB == 3 ? 40 : GW == 4 ? 
       if constexpr (GW == 1) {
         if (pc[k]) wpre[threadIdx.x * wpt + k] = pre;  // only occupied words are ever read
       } else {  // wpt is a multiple of GW (host): groups never straddle threads
-        if (k % GW == 0 && k < wpt) wpre[(threadIdx.x * wpt + k) / GW] = pre;
+        if (k % GW == 0 && k < wpt && threadIdx.x * wpt + k < words) wpre[(threadIdx.x * wpt + k) / GW] = pre;
       }
       pre += pc[k];
     }
@@ -1282,9 +1282,13 @@ static void bin_cells_d(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
   // 2.4 one-CTA TMA, 7.6 bitmap; larger cells at 64^3 take the radix sort.
   const bool bitmap_fits = words * 8 + ccap * 4 + kcap * 4 <= 160 * 1024;
   // 4-word prefix groups when only they bring a large bitmap (64^3) to two CTAs per SM
-  const size_t tma_smem_gw = tma_smem - size_t(words) * 4 + size_t((words + 3) / 4) * 4;
-  const bool gw4 = tb == 512 && words > 8 * 512 && ((words + 511) / 512) % 4 == 0 &&
+  // (the swizzle permutes words within aligned 16-word blocks: the bitmap is padded to a
+  // multiple of 16 words, the padding never set)
+  const int64_t words16 = (words + 15) & ~int64_t(15);
+  const size_t tma_smem_gw = tma_smem - size_t(words) * 8 + size_t(words16) * 4 + size_t(words16 / 4) * 4;
+  const bool gw4 = tb == 512 && words16 > 8 * 512 && ((words16 + 511) / 512) % 4 == 0 &&
                    tma_smem > 110 * 1024 && tma_smem_gw <= 110 * 1024;
+  int kwords = static_cast<int>(words);
   int choice = path_env;
   if (choice == 0 && !weighted) {
     if (tma_fits && (tma_smem <= 110 * 1024 || gw4)) choice = 1;
@@ -1311,6 +1315,7 @@ static void bin_cells_d(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
                               : cells_bitmap_tma_kernel<D, B, WPT, false, 1>)
     if (gw4) {
       tma_smem = tma_smem_gw;
+      kwords = static_cast<int>(words16);
       k = gen ? cells_bitmap_tma_kernel<D, 512, 16, true, 1, false, 4>
               : cells_bitmap_tma_kernel<D, 512, 16, false, 1, false, 4>;
     } else if (tb == 512) {
@@ -1327,7 +1332,7 @@ static void bin_cells_d(vdfcg_ctx* ctx, const CellsDev& c, const CellBinsDev& ou
     const int grid = std::max(1, std::min(c.n_cells, ctx->sm_count * std::max(occ, 1)));
     VelPtrs vp{{c.vel[0], c.vel[1], c.vel[2]}, c.keys};
     VDFCG_LAUNCH(ctx, "cells_bitmap_tma",
-                 k<<<grid, tb, tma_smem, ctx->stream>>>(vp, c.offsets, c.n_cells, g, static_cast<int>(words),
+                 k<<<grid, tb, tma_smem, ctx->stream>>>(vp, c.offsets, c.n_cells, g, kwords,
                                                         static_cast<int>(ccap), static_cast<int>(capp), shift,
                                                         out.nnz, out.keys, out.counts, out.oor, out.in_range));
     done = true;

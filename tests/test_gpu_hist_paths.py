@@ -39,13 +39,15 @@ def test_forced_histogram_path_bit_exact(path, tmp_path):
 
 @pytest.mark.parametrize("n_per_cell,nb,eigen", [(1907, 48, True), (1906, 48, True), (1907, 32, True),
                                                 (1907, 32, False), (1200, 32, False),
-                                                (1907, 64, True), (1907, 64, False)])
+                                                (1907, 64, True), (1907, 64, False),
+                                                (1907, 63, True), (1907, 63, False)])
 def test_tma_path_accepts_eigen_column_bases(n_per_cell, nb, eigen):
     """An Eigen N x 3 column-major matrix with odd N has its v and w columns 8 bytes off a
     16-byte boundary (ParticleSet::velocities, synthdata.hpp:13-28). The TMA kernel carries
     the per-axis skew, so such device columns bin bit-exactly (forced TMA path). 32^3 with
     ~1.9K particles per cell runs the packed-u16-count form (three CTAs per SM), 64^3 the
-    4-word prefix groups (two CTAs per SM), aligned and skewed."""
+    4-word prefix groups (two CTAs per SM), aligned and skewed; 63^3 (7814 bitmap words) the
+    same with the swizzled bitmap padded to a multiple of 16 words."""
     code = f"""
 import sys, numpy as np, torch
 sys.path.insert(0, {ROOT!r})
