@@ -918,7 +918,11 @@ __global__ void __launch_bounds__(BLOCK) __maxnreg__(MINB == 3 ? 40 : GW == 4 ? 
   const int wpt = (words + BLOCK - 1) / BLOCK;
   // GW = 4: word w lives at w ^ ((w >> 5) & 15) — thread t's k-th prefix word 16t + k then
   // hits 32 distinct banks across a warp (a plain stride of 16 words is a 16-way conflict)
+#ifndef VDFCG_HIST_NOSWZ
   auto swz = [](unsigned w) { return GW == 4 ? (w ^ ((w >> 5) & 15u)) : w; };
+#else  // measurement variant only (tools/build_variant.sh hist.cu -DVDFCG_HIST_NOSWZ)
+  auto swz = [](unsigned w) { return w; };
+#endif
   const int64_t lim = offsets[n_cells];
   for (int t = threadIdx.x; t < words; t += BLOCK) bitmap[t] = 0u;
   for (int t = threadIdx.x; t < cw; t += BLOCK) cnt2[t] = 0u;
@@ -1009,7 +1013,7 @@ __global__ void __launch_bounds__(BLOCK) __maxnreg__(MINB == 3 ? 40 : GW == 4 ? 
         } else {
           static_assert(GW == 4, "4-word groups");
           // the group's 4 words sit in one swizzled 16-byte slot, slot p holding word p ^ s3
-          const unsigned sx = (wd >> 5) & 15u, s3 = sx & 3u;
+          const unsigned sx = swz(wd) ^ wd, s3 = sx & 3u;  // the swizzle of this row
           const uint4 q = reinterpret_cast<const uint4*>(bitmap)[((wd & ~3u) ^ (sx & 12u)) >> 2];
           const unsigned j = wd & 3u, lt = (1u << bit) - 1u;
           auto msk = [&](unsigned p) { const unsigned l = p ^ s3; return l < j ? ~0u : l == j ? lt : 0u; };
